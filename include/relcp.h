@@ -1,0 +1,244 @@
+/*
+ * relcp.h -- C ABI of the B200-native ReLCP hot path (arXiv 2506.14097,
+ * "Smooth-Rigid-Body Contact as a ReLCP", Palmer, Aktulga, Gao).
+ *
+ * Library: paper_2506_14097_b200/lib/librelcp.so (CUDA, sm_100a, fp64).
+ *
+ * Citations: P:Lnnn = line of the paper text with the section /
+ * equation in parentheses; R<k> = reading k in DESIGN.md §2.
+ *
+ * Conventions (all calls):
+ *   - every call returns an int status: RELCP_OK (0), an error (< 0) or a
+ *     warning (> 0).  relcp_last_error(ctx) holds a one-line message.
+ *   - every array in relcp_bodies / relcp_constraints is a CALLER-OWNED
+ *     DEVICE pointer (cudaMalloc / torch CUDA tensor), fp64 unless noted,
+ *     contiguous, in the layout stated beside it.  The library never
+ *     allocates or frees caller-visible memory; it owns only its internal
+ *     workspace (cell list, candidate pairs, body-major CSR of D, per-body
+ *     mobility blocks, reduction partials), freed by relcp_destroy.
+ *   - all device work is enqueued on the stream given to relcp_create.
+ *     Calls whose OUTPUT SIZE is data dependent (generate, check/augment,
+ *     step) or that report a host-visible result (solve) synchronise that
+ *     stream before returning; relcp_delassus_apply / relcp_wrench do not.
+ *   - there is no CPU fallback: without a CUDA device every call that does
+ *     work returns RELCP_E_CUDA.
+ *   - results are bitwise deterministic run to run (no floating-point
+ *     atomics; every reduction has a fixed order).
+ *
+ * Notation (§2.1.1, P:L151-157 Eq. collision_ft):
+ *   body b: centre x_b, unit quaternion (s, w), velocity U = (u, w).
+ *   constraint alpha between bodies a = ia < b = ib: outward unit normal n of
+ *   a, lever arms r_a = y_a - x_a, r_b = y_b - x_b at the shared-normal points
+ *   y_a, y_b, torque arms t_a = r_a x n, t_b = r_b x n.
+ *   Row of D^T: [-n, -t_a, n, t_b]   (App. A23; Phi_dot)
+ *   Column of D: wrench -[n; t_a] on a, +[n; t_b] on b (F_a = -n gamma,
+ *   T_a = -(y_a - x_a) x n gamma).
+ *   W_b: M_b^{-1} (inertial) or the local-drag mobility
+ *   (overdamped, Eq. ellipsoid_mobility), frozen at C^k.
+ *   A = s D^T W D, s = dt^2 (inertial) or dt (overdamped).
+ *   LCP: 0 <= g = A lambda + q  _|_  lambda >= 0 (Lemma 3; the
+ *   paper writes b = -q).
+ */
+#ifndef RELCP_H
+#define RELCP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------ status codes */
+#define RELCP_OK 0
+#define RELCP_E_ARG (-1)        /* bad argument (NULL pointer, size, param)  */
+#define RELCP_E_CUDA (-2)       /* CUDA error or no device                   */
+#define RELCP_E_CAPACITY (-3)   /* constraint store too small; see required  */
+#define RELCP_E_DEGENERATE (-4) /* coincident body centres in a pair (R4)    */
+#define RELCP_E_NAN (-5)        /* NaN/Inf in the LCP iterate                */
+#define RELCP_E_STATE (-6)      /* call order violated (e.g. no operator)    */
+#define RELCP_W_MAX_ITER 1      /* LCP stopped at lcp_max_iter, converged=0  */
+#define RELCP_W_RECURSION_CAP 2 /* ReLCP stopped at max_recursions (R15)     */
+#define RELCP_W_SNSD_NONCONV 3  /* some SNSD Newton solves not certified     */
+
+#define RELCP_INERTIAL 0   /* U+ = U + dt M^-1 F  (Eq. law_inertia)   */
+#define RELCP_OVERDAMPED 1 /* U = M F, local drag (Eq. law_overdamped) */
+
+#define RELCP_MAX_REC 64 /* size of the per-recursion arrays in the step report */
+
+typedef struct relcp_ctx relcp_ctx;
+
+/* Parameters.  relcp_default_params fills the values in brackets. */
+typedef struct relcp_params {
+    int32_t dynamics;     /* RELCP_INERTIAL | RELCP_OVERDAMPED [INERTIAL]          */
+    int32_t max_recursions; /* ReLCP recursion cap [50] (R15)                      */
+    double dt;            /* time step [1e-3]                                      */
+    double eps_ncp;       /* overlap tolerance, absolute [1e-5] (R3)       */
+    double cutoff;        /* SNSD cutoff for A_0 [0.1] (R5)         */
+    double lcp_tol;       /* residual tol, r = ||min(lambda, g)||_inf [1e-8] (R2)  */
+    int64_t lcp_max_iter; /* [100000]                                              */
+    int32_t check_every;  /* LCP iterations between host convergence reads [32]    */
+    int32_t power_iters;  /* power iterations for L, alpha_0 = 1/L [20] (R1)       */
+    double box[3];        /* periodic box lengths; 0 = that axis not periodic [0]  */
+    double xi;            /* drag coefficient (overdamped) [1.0]          */
+    int32_t n_dirs;       /* SNSD multistart sample size for overlaps [256] (R4)   */
+    int32_t reserved;
+} relcp_params;
+
+/* Body view (SoA by field, each field row-major per body).
+ *   pos         (n,3)  centre x_b                                  in/out (step)
+ *   quat        (n,4)  unit quaternion (s, wx, wy, wz), P:L66      in/out (step)
+ *   axes        (n,3)  semi-axes (e1, e2, e3) in the body frame    in
+ *   vel         (n,6)  (u, omega), world frame; may be NULL for
+ *                      overdamped bodies                           in/out (step)
+ *   inv_mass    (n)    1/m   (inertial; may be NULL if overdamped) in
+ *   inv_inertia (n,3)  1/I_k, principal body-frame (inertial)      in
+ *   kinematic   (n) int32, 1 = prescribed velocity (W_b = 0); NULL = none */
+typedef struct relcp_bodies {
+    int64_t n;
+    double *pos;
+    double *quat;
+    const double *axes;
+    double *vel;
+    const double *inv_mass;
+    const double *inv_inertia;
+    const int32_t *kinematic;
+} relcp_bodies;
+
+/* Constraint store: SoA, append-only within a step (App. D1).
+ *   count        host-side element count (in/out; library updates it).
+ *   ia, ib, gen  (capacity) int32: body ids (ia < ib) and the recursion index
+ *                that appended the row (0 = A_0).  Within a generation block
+ *                rows are sorted by (ia, ib) (R18).
+ *   n, ta, tb    (3, capacity) planes: component k of row alpha at
+ *                [k*capacity + alpha]; unit normal n, torque arms t_a, t_b
+ *                frozen at the discovery configuration (R9).
+ *   phi          (capacity) signed distance at the discovery configuration.
+ *   q            (capacity) LCP right-hand side (q = -b).
+ *   lambda       (capacity) multipliers gamma (in: warm start; out: solution).
+ *   g            (capacity) gap g = A lambda + q written by the solver; may be
+ *                NULL for calls that do not solve. */
+typedef struct relcp_constraints {
+    int64_t capacity;
+    int64_t count;
+    int32_t *ia, *ib, *gen;
+    double *n, *ta, *tb;
+    double *phi, *q, *lambda, *g;
+} relcp_constraints;
+
+typedef struct relcp_solve_report {
+    int64_t iterations; /* BB projected-gradient iterations (R1)             */
+    double residual;    /* ||min(lambda, g)||_inf at exit (R2)                */
+    int32_t converged;  /* residual <= lcp_tol                                */
+    int32_t pad;
+    double objective;   /* f = -1/2 lambda^T A lambda          */
+    double L;           /* power-iteration estimate of ||A||_2                 */
+} relcp_solve_report;
+
+typedef struct relcp_step_report {
+    int32_t recursions;                 /* augmentations performed (n of Alg. 1) */
+    int32_t status;                     /* 0 | RELCP_W_RECURSION_CAP             */
+    int64_t n_pairs;                    /* candidate pairs at the final margin   */
+    double margin;                      /* final broadphase margin (R7)          */
+    double max_overlap;                 /* max(0, -min Phi) at the accepted C    */
+    int64_t n_c[RELCP_MAX_REC];         /* N_C of LCP n                          */
+    int64_t lcp_iters[RELCP_MAX_REC];   /* iterations of LCP n                   */
+    double residual[RELCP_MAX_REC];     /* residual of LCP n                     */
+    double f_n[RELCP_MAX_REC];          /* f_n = -1/2 x^T A_n x        */
+    double ms_generate, ms_solve, ms_check; /* wall time per phase (events)      */
+    int64_t snsd_nonconv;               /* SNSD solves not certified (all calls) */
+} relcp_step_report;
+
+/* ---------------------------------------------------------------- context */
+
+/* Fill *p with the defaults listed in relcp_params. */
+void relcp_default_params(relcp_params *p);
+
+/* Create a context bound to `cuda_stream` (a cudaStream_t; NULL = legacy
+ * default stream).  Errors: E_ARG (p NULL or invalid), E_CUDA. */
+int relcp_create(relcp_ctx **out, const relcp_params *p, void *cuda_stream);
+int relcp_destroy(relcp_ctx *ctx);
+const char *relcp_last_error(const relcp_ctx *ctx);
+/* Replace the parameters (e.g. dt or box between steps). */
+int relcp_set_params(relcp_ctx *ctx, const relcp_params *p);
+
+/* ------------------------------------------------------------- hot path */
+
+/* a1-a3: broadphase (cell list, candidate pairs with
+ *   |x_b - x_a|_min-image < R_a + R_b + cutoff, R = largest semi-axis;
+ *   "near-contacting pairs"), SNSD of every pair at the
+ *   bodies' configuration (definition R4), and the A_0 rows
+ *   of pairs with Phi < cutoff (R5), appended in (ia, ib) order with gen = 0,
+ *   lambda = 0 and q = Phi + dt row.U_free, U_free = vel (inertial,
+ *   P:L557-561; F_ext = 0 here) or 0 (overdamped).
+ *   The store is RESET (count = 0) first.  *n_out = rows written.
+ *   Keeps the candidate pairs, W and U_free in the context for
+ *   relcp_check_and_augment.  Synchronises once.
+ * Errors: E_CAPACITY (cs->count = required rows, nothing written),
+ *   E_DEGENERATE; warning W_SNSD_NONCONV. */
+int relcp_generate_contacts(relcp_ctx *ctx, const relcp_bodies *bodies, relcp_constraints *cs,
+                            int64_t *n_out);
+
+/* Build the operator for the current store: per-body W blocks at the bodies'
+ * configuration (frozen C^k) and the body-major CSR of D.  Must be called
+ * again after the caller edits ia/ib/n/ta/tb/count.  Generate, solve,
+ * check/augment and step (re)build it themselves. */
+int relcp_prepare_operator(relcp_ctx *ctx, const relcp_bodies *bodies, const relcp_constraints *cs);
+
+/* a5: y = scale * D^T W D x for the prepared operator (P:L154-157, P:L207-211,
+ * P:L627).  x, y: device, length cs->count (may not alias).  Asynchronous.
+ * Errors: E_ARG, E_STATE (operator not prepared for this count). */
+int relcp_delassus_apply(relcp_ctx *ctx, const relcp_bodies *bodies, const relcp_constraints *cs,
+                         const double *x, double *y, double scale);
+
+/* Body wrench F = D x and velocity U = W D x, (n,6) each, either may be NULL.
+ * Asynchronous.  Errors as relcp_delassus_apply. */
+int relcp_wrench(relcp_ctx *ctx, const relcp_bodies *bodies, const relcp_constraints *cs,
+                 const double *x, double *F, double *U);
+
+/* a6: solve 0 <= A lambda + q _|_ lambda >= 0 in place (Lemma 3, P:L280-299;
+ * Barzilai-Borwein projected gradient, R1).  lambda in = warm start
+ * (projected onto lambda >= 0), out = solution; cs->g = A lambda + q.
+ * Prepares the operator if needed.  Synchronises once per check_every
+ * iterations.  Warning W_MAX_ITER (last iterate returned); error E_NAN. */
+int relcp_solve_lcp(relcp_ctx *ctx, const relcp_bodies *bodies, relcp_constraints *cs,
+                    relcp_solve_report *rep);
+
+/* a7-a8: trial configuration C_{n+1} = C^k + dt G^k U_tot, U_tot = U_free +
+ * sigma W D lambda (sigma = dt inertial, 1 overdamped, R6),
+ * SNSD of the context's candidate pairs at C_{n+1} (margin widened per R7),
+ * and append of every pair with Phi < -eps_ncp (R10) with gen =
+ * `recursion`, geometry frozen at C_{n+1} (R9), lambda = 0 and
+ * q = Phi - s row.(W D lambda) (Thm 1 RHS b_n = A_n iota(x_{n-1}) - g~,
+ * P:L587; retained q unchanged).  *n_appended = 0 <=> stopping rule
+ * (P:L646-648).  *min_phi = min Phi over the pairs at C_{n+1}.
+ * `Ck` = the bodies at the start of the step (unchanged).  Requires a prior
+ * relcp_generate_contacts on the same bodies.  Synchronises.
+ * Errors: E_STATE, E_CAPACITY (cs->count = required rows), E_DEGENERATE. */
+int relcp_check_and_augment(relcp_ctx *ctx, const relcp_bodies *Ck, relcp_constraints *cs,
+                            int32_t recursion, int64_t *n_appended, double *min_phi);
+
+/* One ReLCP time step: Algorithm 1, inertial form Eq.
+ * relcp_inertial.  f_ext: (n,6) device or NULL (= 0).  Updates
+ * pos (wrapped into the periodic box), quat (normalised) and vel in place:
+ * C^{k+1} = accepted trial configuration, U^{k+1} = U_free + sigma W D lambda.
+ * `scratch` is the constraint store used for the step (its final content is
+ * the step's A_c).  Warning W_RECURSION_CAP (the last trial configuration is
+ * accepted and flagged). */
+int relcp_step(relcp_ctx *ctx, relcp_bodies *inout, const double *f_ext, relcp_constraints *scratch,
+               relcp_step_report *rep);
+
+/* Candidate pairs currently held by the context (after generate / augment):
+ * *n_pairs = count; if pi/pj non-NULL (device, capacity cap) they receive the
+ * pairs in (i, j) lexicographic order.  Synchronises. */
+int relcp_get_pairs(relcp_ctx *ctx, int32_t *pi, int32_t *pj, int64_t cap, int64_t *n_pairs);
+
+/* SNSD of explicit pairs (device arrays, length n_pairs) at the given bodies:
+ * phi (P), nrm (3,P) planes, ra (3,P), rb (3,P) planes (r = y - x), status
+ * (P) int32 0 ok / 1 coincident centres / 2 not certified.  Asynchronous. */
+int relcp_snsd_pairs(relcp_ctx *ctx, const relcp_bodies *bodies, int64_t n_pairs, const int32_t *pi,
+                     const int32_t *pj, double *phi, double *nrm, double *ra, double *rb, int32_t *status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RELCP_H */

@@ -1,0 +1,160 @@
+// Internal header of librelcp.so (B200 / sm_100a, fp64).  Not part of the ABI.
+// Citations: P:Lnnn = paper line; R<k> = DESIGN.md reading k.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdarg.h>
+#include <string.h>
+
+#include "../../include/relcp.h"
+
+#define RELCP_NT 256          // threads per block for streaming kernels
+#define RELCP_SM_COUNT 148    // B200
+#define RELCP_MAX_DIRS 1024   // cap on the SNSD start sample
+
+// ------------------------------------------------------------ device buffer
+template <class T>
+struct DevBuf {
+    T *p = nullptr;
+    size_t cap = 0;  // elements
+    cudaError_t grow(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = n + n / 4 + 64;
+        cudaError_t e = cudaMalloc((void **)&p, want * sizeof(T));
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+// Device-side state of one LCP solve (BB projected gradient, R1).
+struct LcpState {
+    double alpha;   // current step length
+    double L;       // ||A|| estimate (power iteration)
+    double resid;   // ||min(x, g)||_inf of the current iterate
+    double ss, sy, yy;
+    double obj;     // x^T (g - q) = x^T A x
+    double pnorm;   // power iteration: scale applied to the input vector
+    double tol;
+    long long iter;     // completed BB iterations
+    long long max_iter;
+    int done;
+    int conv;
+    int nan;
+    int pad;
+};
+
+// Per-body mobility block W_b in a single 7-double form:
+//   U_lin = w[0] * F_lin ;  U_ang = S F_ang, S symmetric = {w1..w6} =
+//   (xx, xy, xz, yy, yz, zz).  Inertial: w0 = 1/m, S = R I^-1 R^T;
+//   overdamped local drag: w0 = 1/(xi L), S = 12/(xi L^3) I.
+#define RELCP_WSTRIDE 8
+
+struct relcp_ctx {
+    relcp_params p;
+    cudaStream_t stream;
+    char err[512];
+
+    // operator (prepared for `op_nc` rows and `op_nb` bodies)
+    int64_t op_nc = -1, op_nb = -1;
+    const void *op_key_ia = nullptr;
+    DevBuf<double> W;        // (nb, 8)
+    DevBuf<int> row_ptr;     // (nb + 1)
+    DevBuf<int> deg;         // (nb)  scratch
+    DevBuf<int> fill;        // (nb)  scratch
+    DevBuf<int> ecid;        // (2 nc) constraint index of each half entry (body-major)
+    DevBuf<double> ew;       // (6, 2 nc) signed wrench payload, body-major
+    DevBuf<double> U;        // (nb, 6) U = W D x of the last scatter
+    DevBuf<double> F;        // (nb, 6) scratch for relcp_wrench
+    DevBuf<double> partials; // (blocks, 4)
+    DevBuf<unsigned> counter;
+    DevBuf<LcpState> st;
+    DevBuf<double> vtmp;     // (nc) power iteration / apply scratch
+    LcpState *st_host = nullptr;  // pinned mirror
+
+    // step state (from generate_contacts at C^k)
+    int64_t step_nb = -1;
+    const double *step_pos_key = nullptr;
+    DevBuf<int> pi, pj;      // candidate pairs
+    int64_t npairs = 0;
+    double margin = 0.0;
+    DevBuf<double> Sig;      // (nb, 6) shape matrices at the config being tested
+    DevBuf<double> ufree;    // (nb, 6)
+    DevBuf<double> utot;     // (nb, 6)
+    DevBuf<double> ptrial;   // (nb, 3)
+    DevBuf<double> qtrial;   // (nb, 4)
+    DevBuf<double> rad;      // (nb)
+    // pair temporaries
+    DevBuf<double> tphi, tn, tra, trb;  // (P), (3,P) planes
+    DevBuf<int> tflag, tstat;
+    DevBuf<long long> scan_ll;  // scan scratch
+    DevBuf<long long> scan_tmp;
+    DevBuf<int> cell_count, cell_start, cell_fill, cell_items, body_cell;
+    DevBuf<long long> pair_cnt;  // per body pair counts (then offsets)
+    DevBuf<double> red;          // small reduction buffer
+    double *red_host = nullptr;  // pinned (64 doubles)
+    int64_t snsd_nonconv_total = 0;
+};
+
+// ------------------------------------------------------------ error helpers
+int set_err(relcp_ctx *c, int code, const char *fmt, ...);
+
+#define CK(call)                                                                   \
+    do {                                                                           \
+        cudaError_t e_ = (call);                                                   \
+        if (e_ != cudaSuccess)                                                     \
+            return set_err(ctx, RELCP_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, \
+                           cudaGetErrorString(e_));                                \
+    } while (0)
+
+#define CKL()                                                                      \
+    do {                                                                           \
+        cudaError_t e_ = cudaGetLastError();                                       \
+        if (e_ != cudaSuccess)                                                     \
+            return set_err(ctx, RELCP_E_CUDA, "%s:%d launch: %s", __FILE__, __LINE__, \
+                           cudaGetErrorString(e_));                                \
+    } while (0)
+
+#define CKS(expr)                  \
+    do {                           \
+        int s_ = (expr);           \
+        if (s_ < 0) return s_;     \
+    } while (0)
+
+static inline int grid_for(int64_t n, int nt = RELCP_NT, int per_sm = 8) {
+    int64_t g = (n + nt - 1) / nt;
+    int64_t cap = (int64_t)RELCP_SM_COUNT * per_sm;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+// ------------------------------------------------------------ internal API
+// operator.cu
+int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *cs);
+int op_build_W(relcp_ctx *ctx, const relcp_bodies *b, double *W);
+// scatter (+ optional BB projection) followed by W: U = W D xeff
+int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int proj,
+               const double *xscale_dev, double *U, double *F);
+int op_gather_apply(relcp_ctx *ctx, const relcp_constraints *cs, const double *U, double *y, double scale,
+                    int norm2);
+int op_row_dot_U(relcp_ctx *ctx, const relcp_constraints *cs, int64_t begin, int64_t end, const double *U,
+                 double coef, double *out_add);
+// lcp.cu
+int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relcp_solve_report *rep);
+// scan.cu
+int scan_exclusive_ll(relcp_ctx *ctx, const long long *in, long long *out, int64_t n, long long *total_host);
+int scan_exclusive_int(relcp_ctx *ctx, const int *in, int *out, int64_t n, int *total_host);
+// geometry.cu
+int geo_shape_matrices(relcp_ctx *ctx, int64_t nb, const double *quat, const double *axes, double *Sig);
+int geo_broadphase(relcp_ctx *ctx, int64_t nb, const double *pos, const double *rad, double margin);
+int geo_snsd(relcp_ctx *ctx, int64_t np, const int *pi, const int *pj, const double *pos, const double *Sig,
+             double *phi, double *nrm, double *ra, double *rb, int *status, int64_t planes);

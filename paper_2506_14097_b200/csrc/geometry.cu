@@ -1,0 +1,490 @@
+// Geometry kernels: ellipsoid shape matrices, cell-list broadphase (K1/K2)
+// and the batched shared-normal signed distance (K3/K10).
+//
+// SNSD ("the points that minimize their shared-normal signed
+// separation distance"; W-W formulation cited at P:L944, not given; reading
+// R4): for ellipsoids with Sigma = R diag(e^2) R^T and support function
+// h(n) = sqrt(n^T Sigma n),
+//     Phi = max_{|n|=1} F(n),  F(n) = n.d - h_a(n) - h_b(n),  d = x_b - x_a,
+//     y_a = x_a + Sigma_a n / h_a,  y_b = x_b - Sigma_b n / h_b.
+// At a stationary point y_b - y_a = Phi n.
+//
+// GPU strategy (differs from the oracle's fixed multistart):
+//   F is concave and positively homogeneous on R^3, so a local maximum on the
+//   sphere with F > 0 is the global one.  Each thread first runs damped
+//   Riemannian Newton from d/|d|; only if that ends with F <= 0 (overlap or
+//   touching) does it sample `n_dirs` Fibonacci directions and restart Newton
+//   from the best four, keeping the largest maximum (ties: larger n.d/|d|,
+//   then lexicographically smaller n; R4).
+#include "common.cuh"
+#include "reduce.cuh"
+
+// ------------------------------------------------------------ shape matrices
+// Sig (nb, 6) = (xx, xy, xz, yy, yz, zz) of R diag(e^2) R^T, q normalised.
+__global__ void k_shape(int64_t nb, const double *__restrict__ quat, const double *__restrict__ axes,
+                        double *__restrict__ Sig) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        double s = quat[4 * b], x = quat[4 * b + 1], y = quat[4 * b + 2], z = quat[4 * b + 3];
+        double inv = 1.0 / sqrt(s * s + x * x + y * y + z * z);
+        s *= inv; x *= inv; y *= inv; z *= inv;
+        const double R[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - s * z), 2 * (x * z + s * y)},
+                                {2 * (x * y + s * z), 1 - 2 * (x * x + z * z), 2 * (y * z - s * x)},
+                                {2 * (x * z - s * y), 2 * (y * z + s * x), 1 - 2 * (x * x + y * y)}};
+        const double e0 = axes[3 * b] * axes[3 * b], e1 = axes[3 * b + 1] * axes[3 * b + 1],
+                     e2 = axes[3 * b + 2] * axes[3 * b + 2];
+        auto S = [&](int i, int j) { return R[i][0] * e0 * R[j][0] + R[i][1] * e1 * R[j][1] + R[i][2] * e2 * R[j][2]; };
+        double *o = Sig + 6 * b;
+        o[0] = S(0, 0); o[1] = S(0, 1); o[2] = S(0, 2);
+        o[3] = S(1, 1); o[4] = S(1, 2); o[5] = S(2, 2);
+    }
+}
+
+int geo_shape_matrices(relcp_ctx *ctx, int64_t nb, const double *quat, const double *axes, double *Sig) {
+    k_shape<<<grid_for(nb), RELCP_NT, 0, ctx->stream>>>(nb, quat, axes, Sig);
+    CKL();
+    return RELCP_OK;
+}
+
+// ------------------------------------------------------------ SNSD device code
+struct Sym {
+    double xx, xy, xz, yy, yz, zz;
+};
+__device__ __forceinline__ Sym load_sym(const double *__restrict__ p) {
+    Sym s;
+    s.xx = p[0]; s.xy = p[1]; s.xz = p[2]; s.yy = p[3]; s.yz = p[4]; s.zz = p[5];
+    return s;
+}
+__device__ __forceinline__ void smv(const Sym &S, const double *v, double *o) {
+    o[0] = S.xx * v[0] + S.xy * v[1] + S.xz * v[2];
+    o[1] = S.xy * v[0] + S.yy * v[1] + S.yz * v[2];
+    o[2] = S.xz * v[0] + S.yz * v[1] + S.zz * v[2];
+}
+__device__ __forceinline__ double d3(const double *a, const double *b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+
+struct Eval {
+    double f, ha, hb;
+    double Sa_n[3], Sb_n[3], v[3];  // v = d - Sa n/ha - Sb n/hb (= y_b - y_a)
+};
+
+__device__ __forceinline__ void feval(const double *n, const double *d, const Sym &Sa, const Sym &Sb, Eval &E) {
+    smv(Sa, n, E.Sa_n);
+    smv(Sb, n, E.Sb_n);
+    E.ha = sqrt(d3(n, E.Sa_n));
+    E.hb = sqrt(d3(n, E.Sb_n));
+    E.f = d3(n, d) - E.ha - E.hb;
+    const double ia = 1.0 / E.ha, ib = 1.0 / E.hb;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) E.v[k] = d[k] - E.Sa_n[k] * ia - E.Sb_n[k] * ib;
+}
+
+__device__ __forceinline__ double fval(const double *n, const double *d, const Sym &Sa, const Sym &Sb) {
+    double t[3];
+    smv(Sa, n, t);
+    double ha = sqrt(d3(n, t));
+    smv(Sb, n, t);
+    double hb = sqrt(d3(n, t));
+    return d3(n, d) - ha - hb;
+}
+
+// t^T (S/h - (S n)(S n)^T / h^3) u  for the support-function Hessian
+__device__ __forceinline__ double hess_form(const Sym &S, const double *Sn, double h, const double *t, const double *u) {
+    double Su[3];
+    smv(S, u, Su);
+    return d3(t, Su) / h - d3(t, Sn) * d3(u, Sn) / (h * h * h);
+}
+
+// Damped Riemannian Newton ascent of F on the unit sphere from n (in/out).
+// Returns 1 if certified (gradient or step at the rounding floor).
+__device__ int newton_sphere(double *n, const double *d, double dnorm, const Sym &Sa, const Sym &Sb, Eval &E) {
+    const double gtol = 1e-13 * fmax(1.0, dnorm);
+    feval(n, d, Sa, Sb, E);
+    for (int it = 0; it < 64; ++it) {
+        // tangent frame: t1 from the coordinate axis least aligned with n
+        const double ax = fabs(n[0]), ay = fabs(n[1]), az = fabs(n[2]);
+        double e[3] = {0.0, 0.0, 0.0};
+        if (ax <= ay && ax <= az) e[0] = 1.0; else if (ay <= az) e[1] = 1.0; else e[2] = 1.0;
+        const double ne = d3(n, e);
+        double t1[3] = {e[0] - ne * n[0], e[1] - ne * n[1], e[2] - ne * n[2]};
+        const double il = 1.0 / sqrt(d3(t1, t1));
+        t1[0] *= il; t1[1] *= il; t1[2] *= il;
+        const double t2[3] = {n[1] * t1[2] - n[2] * t1[1], n[2] * t1[0] - n[0] * t1[2], n[0] * t1[1] - n[1] * t1[0]};
+        const double g1 = d3(t1, E.v), g2 = d3(t2, E.v);
+        if (sqrt(g1 * g1 + g2 * g2) <= gtol) return 1;
+        const double nv = d3(n, E.v);
+        // Riemannian Hessian in the (t1, t2) frame: P Hess(F) P - (n . grad F) I
+        const double h11 = -hess_form(Sa, E.Sa_n, E.ha, t1, t1) - hess_form(Sb, E.Sb_n, E.hb, t1, t1) - nv;
+        const double h22 = -hess_form(Sa, E.Sa_n, E.ha, t2, t2) - hess_form(Sb, E.Sb_n, E.hb, t2, t2) - nv;
+        const double h12 = -0.5 * (hess_form(Sa, E.Sa_n, E.ha, t1, t2) + hess_form(Sa, E.Sa_n, E.ha, t2, t1)) -
+                           0.5 * (hess_form(Sb, E.Sb_n, E.hb, t1, t2) + hess_form(Sb, E.Sb_n, E.hb, t2, t1));
+        const double scale = fabs(h11) + fabs(h12) + fabs(h22) + 1e-300;
+        const double lmax = 0.5 * (h11 + h22) + sqrt(0.25 * (h11 - h22) * (h11 - h22) + h12 * h12);
+        double mu = lmax > -1e-8 * scale ? lmax + 1e-8 * scale + 1e-12 : 0.0;
+        bool accepted = false;
+        double step = 0.0;
+        Eval En;
+        double nn[3];
+        for (int tr = 0; tr < 48; ++tr) {
+            const double a = h11 - mu, c = h22 - mu;
+            const double det = a * c - h12 * h12;
+            double x1 = -(c * g1 - h12 * g2) / det;
+            double x2 = -(a * g2 - h12 * g1) / det;
+            double xl = sqrt(x1 * x1 + x2 * x2);
+            if (xl > 0.5) {
+                x1 *= 0.5 / xl;
+                x2 *= 0.5 / xl;
+                xl = 0.5;
+            }
+            nn[0] = n[0] + x1 * t1[0] + x2 * t2[0];
+            nn[1] = n[1] + x1 * t1[1] + x2 * t2[1];
+            nn[2] = n[2] + x1 * t1[2] + x2 * t2[2];
+            const double inn = 1.0 / sqrt(d3(nn, nn));
+            nn[0] *= inn; nn[1] *= inn; nn[2] *= inn;
+            feval(nn, d, Sa, Sb, En);
+            if (En.f >= E.f - 1e-15 * (1.0 + dnorm)) {
+                accepted = true;
+                step = xl;
+                break;
+            }
+            mu = 4.0 * mu + scale + 1e-12;
+        }
+        if (!accepted) return 1;  // no ascent left at rounding level
+        n[0] = nn[0]; n[1] = nn[1]; n[2] = nn[2];
+        E = En;
+        if (step < 1e-14) return 1;
+    }
+    return 0;
+}
+
+__device__ __forceinline__ bool better(double f, const double *n, double fb, const double *nb, const double *dh) {
+    if (f > fb) return true;
+    if (f < fb) return false;
+    const double c1 = d3(n, dh), c0 = d3(nb, dh);
+    if (c1 != c0) return c1 > c0;
+    if (n[0] != nb[0]) return n[0] < nb[0];
+    if (n[1] != nb[1]) return n[1] < nb[1];
+    return n[2] < nb[2];
+}
+
+// Full SNSD of one pair.  Returns status 0 ok / 1 coincident / 2 not certified.
+__device__ int snsd_pair(const double *d, const Sym &Sa, const Sym &Sb, int n_dirs, double &phi, double *nout,
+                         double *ra, double *rb) {
+    const double dn = sqrt(d3(d, d));
+    if (!(dn >= 1e-12)) {
+        phi = nan("");
+        for (int k = 0; k < 3; ++k) nout[k] = ra[k] = rb[k] = nan("");
+        return 1;
+    }
+    const double dh[3] = {d[0] / dn, d[1] / dn, d[2] / dn};
+    double nb[3] = {dh[0], dh[1], dh[2]};
+    Eval Eb;
+    int st_best = newton_sphere(nb, d, dn, Sa, Sb, Eb) ? 0 : 2;
+    double fb = Eb.f;
+    if (!(fb > 0.0)) {
+        // overlap / touching: multistart from the best sampled directions
+        constexpr int K = 4;
+        double topf[K];
+        int topi[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) { topf[k] = -INFINITY; topi[k] = -1; }
+        const double ga = 3.14159265358979323846 * (3.0 - sqrt(5.0));
+        for (int i = 0; i < n_dirs; ++i) {
+            const double z = 1.0 - (2.0 * i + 1.0) / n_dirs;
+            const double r = sqrt(fmax(0.0, 1.0 - z * z));
+            double sn, cs;
+            sincos(ga * i, &sn, &cs);
+            const double m[3] = {r * cs, r * sn, z};
+            const double f = fval(m, d, Sa, Sb);
+            if (f > topf[K - 1]) {
+                int p = K - 1;
+                while (p > 0 && topf[p - 1] < f) {
+                    topf[p] = topf[p - 1];
+                    topi[p] = topi[p - 1];
+                    --p;
+                }
+                topf[p] = f;
+                topi[p] = i;
+            }
+        }
+        for (int k = 0; k < K; ++k) {
+            if (topi[k] < 0) continue;
+            const int i = topi[k];
+            const double z = 1.0 - (2.0 * i + 1.0) / n_dirs;
+            const double r = sqrt(fmax(0.0, 1.0 - z * z));
+            double sn, cs;
+            sincos(ga * i, &sn, &cs);
+            double m[3] = {r * cs, r * sn, z};
+            Eval Em;
+            int ok = newton_sphere(m, d, dn, Sa, Sb, Em);
+            if (better(Em.f, m, fb, nb, dh)) {
+                fb = Em.f;
+                nb[0] = m[0]; nb[1] = m[1]; nb[2] = m[2];
+                Eb = Em;
+                st_best = ok ? 0 : 2;
+            }
+        }
+    }
+    feval(nb, d, Sa, Sb, Eb);
+    phi = Eb.f;
+    const double ia = 1.0 / Eb.ha, ib = 1.0 / Eb.hb;
+    for (int k = 0; k < 3; ++k) {
+        nout[k] = nb[k];
+        ra[k] = Eb.Sa_n[k] * ia;
+        rb[k] = -Eb.Sb_n[k] * ib;
+    }
+    return st_best;
+}
+
+__device__ __forceinline__ void min_image(const double *xa, const double *xb, const double *box, double *d) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double t = xb[k] - xa[k];
+        if (box[k] > 0.0) t -= box[k] * rint(t / box[k]);
+        d[k] = t;
+    }
+}
+
+struct Box3 {
+    double v[3];
+};
+
+// Batched SNSD over pairs; outputs as planes with stride `planes`.
+__global__ void __launch_bounds__(128) k_snsd(int64_t np, const int *__restrict__ pi, const int *__restrict__ pj,
+                                              const double *__restrict__ pos, const double *__restrict__ Sig,
+                                              Box3 box, int n_dirs, double *__restrict__ phi,
+                                              double *__restrict__ nrm, double *__restrict__ ra,
+                                              double *__restrict__ rb, int *__restrict__ status, int64_t planes) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < np; k += (int64_t)gridDim.x * blockDim.x) {
+        const int a = pi[k], b = pj[k];
+        double d[3];
+        min_image(pos + 3 * (int64_t)a, pos + 3 * (int64_t)b, box.v, d);
+        const Sym Sa = load_sym(Sig + 6 * (int64_t)a), Sb = load_sym(Sig + 6 * (int64_t)b);
+        double f, n[3], r1[3], r2[3];
+        int st = snsd_pair(d, Sa, Sb, n_dirs, f, n, r1, r2);
+        phi[k] = f;
+        for (int c = 0; c < 3; ++c) {
+            nrm[c * planes + k] = n[c];
+            ra[c * planes + k] = r1[c];
+            rb[c * planes + k] = r2[c];
+        }
+        status[k] = st;
+    }
+}
+
+int geo_snsd(relcp_ctx *ctx, int64_t np, const int *pi, const int *pj, const double *pos, const double *Sig,
+             double *phi, double *nrm, double *ra, double *rb, int *status, int64_t planes) {
+    if (np <= 0) return RELCP_OK;
+    Box3 bx;
+    for (int k = 0; k < 3; ++k) bx.v[k] = ctx->p.box[k];
+    int nd = ctx->p.n_dirs > 0 ? ctx->p.n_dirs : 256;
+    if (nd > RELCP_MAX_DIRS) nd = RELCP_MAX_DIRS;
+    int64_t g = (np + 127) / 128;
+    if (g > 148 * 64) g = 148 * 64;
+    k_snsd<<<(unsigned)g, 128, 0, ctx->stream>>>(np, pi, pj, pos, Sig, bx, nd, phi, nrm, ra, rb, status, planes);
+    CKL();
+    return RELCP_OK;
+}
+
+// ------------------------------------------------------------ broadphase
+struct Grid {
+    int nc[3];
+    double lo[3];
+    double cs[3];     // cell edge per axis
+    double box[3];    // > 0: periodic
+};
+
+__device__ __forceinline__ int cell_coord(double x, const Grid &G, int k) {
+    int c;
+    if (G.box[k] > 0.0) {
+        double u = x / G.box[k];
+        u -= floor(u);
+        c = (int)(u * G.nc[k]);
+    } else {
+        c = (int)floor((x - G.lo[k]) / G.cs[k]);
+    }
+    return c < 0 ? 0 : (c >= G.nc[k] ? G.nc[k] - 1 : c);
+}
+
+// body -> cell; per-cell counts (integer atomics: exact counts)
+__global__ void k_cell_assign(int64_t nb, const double *__restrict__ pos, Grid G, int *__restrict__ body_cell,
+                              int *__restrict__ cell_count) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        int cx = cell_coord(pos[3 * b], G, 0), cy = cell_coord(pos[3 * b + 1], G, 1), cz = cell_coord(pos[3 * b + 2], G, 2);
+        int c = (cz * G.nc[1] + cy) * G.nc[0] + cx;
+        body_cell[b] = c;
+        atomicAdd(cell_count + c, 1);
+    }
+}
+
+__global__ void k_cell_fill(int64_t nb, const int *__restrict__ body_cell, const int *__restrict__ cell_start,
+                            int *__restrict__ cell_fill, int *__restrict__ items) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        int c = body_cell[b];
+        items[cell_start[c] + atomicAdd(cell_fill + c, 1)] = (int)b;
+    }
+}
+
+// Unique neighbour cells along one axis (periodic wrap or clipped).
+__device__ __forceinline__ int axis_neighbours(int c, int k, const Grid &G, int *out) {
+    int m = 0;
+    for (int o = -1; o <= 1; ++o) {
+        int v = c + o;
+        if (G.box[k] > 0.0) {
+            v = (v % G.nc[k] + G.nc[k]) % G.nc[k];
+        } else if (v < 0 || v >= G.nc[k]) {
+            continue;
+        }
+        bool dup = false;
+        for (int t = 0; t < m; ++t) dup |= out[t] == v;
+        if (!dup) out[m++] = v;
+    }
+    return m;
+}
+
+__device__ __forceinline__ bool near_pair(const double *__restrict__ pos, const double *__restrict__ rad,
+                                          const Grid &G, double margin, int i, int j) {
+    double d[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double t = pos[3 * (int64_t)j + k] - pos[3 * (int64_t)i + k];
+        if (G.box[k] > 0.0) t -= G.box[k] * rint(t / G.box[k]);
+        d[k] = t;
+    }
+    const double r = rad[i] + rad[j] + margin;
+    return d[0] * d[0] + d[1] * d[1] + d[2] * d[2] < r * r;
+}
+
+// pass 0: count pairs (i < j) per body; pass 1: write them, sorted by j.
+template <int PASS>
+__global__ void __launch_bounds__(128) k_pairs2(int64_t nb, const double *__restrict__ pos,
+                                                const double *__restrict__ rad, Grid G, double margin,
+                                                const int *__restrict__ body_cell, const int *__restrict__ cell_start,
+                                                const int *__restrict__ cell_count, const int *__restrict__ items,
+                                                long long *__restrict__ cnt_or_off, int *__restrict__ pi,
+                                                int *__restrict__ pj) {
+    for (int64_t ib = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ib < nb; ib += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)ib;
+        const int c = body_cell[i];
+        const int cx = c % G.nc[0], cy = (c / G.nc[0]) % G.nc[1], cz = c / (G.nc[0] * G.nc[1]);
+        int nx[3], ny[3], nz[3];
+        const int mx = axis_neighbours(cx, 0, G, nx), my = axis_neighbours(cy, 1, G, ny),
+                  mz = axis_neighbours(cz, 2, G, nz);
+        long long m = 0;
+        const long long base = PASS == 1 ? cnt_or_off[i] : 0;
+        for (int a = 0; a < mz; ++a)
+            for (int b2 = 0; b2 < my; ++b2)
+                for (int e = 0; e < mx; ++e) {
+                    const int cc = (nz[a] * G.nc[1] + ny[b2]) * G.nc[0] + nx[e];
+                    const int s = cell_start[cc], t = s + cell_count[cc];
+                    for (int q = s; q < t; ++q) {
+                        const int j = items[q];
+                        if (j <= i) continue;
+                        if (!near_pair(pos, rad, G, margin, i, j)) continue;
+                        if (PASS == 1) {
+                            pi[base + m] = i;
+                            pj[base + m] = j;
+                        }
+                        ++m;
+                    }
+                }
+        if (PASS == 0) {
+            cnt_or_off[i] = m;
+        } else {
+            // insertion sort of this body's partners: lexicographic (i, j) order
+            for (long long u = base + 1; u < base + m; ++u) {
+                int k = pj[u];
+                long long v = u - 1;
+                while (v >= base && pj[v] > k) {
+                    pj[v + 1] = pj[v];
+                    --v;
+                }
+                pj[v + 1] = k;
+            }
+        }
+    }
+}
+
+// bounds: min pos (3), max pos (3), max rad
+__global__ void __launch_bounds__(RELCP_NT) k_bounds(int64_t nb, const double *__restrict__ pos,
+                                                     const double *__restrict__ rad, double *part,
+                                                     unsigned *counter, double *out) {
+    __shared__ double sh[7 * 32];
+    double v[7] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY, 0.0};
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        for (int k = 0; k < 3; ++k) {
+            v[k] = fmin(v[k], pos[3 * b + k]);
+            v[3 + k] = fmax(v[3 + k], pos[3 * b + k]);
+        }
+        v[6] = fmax(v[6], rad[b]);
+    }
+    const int ops[7] = {2, 2, 2, 1, 1, 1, 1};
+    if (grid_reduce_last<7>(v, ops, part, counter, sh) && threadIdx.x == 0)
+        for (int k = 0; k < 7; ++k) out[k] = v[k];
+}
+
+int geo_broadphase(relcp_ctx *ctx, int64_t nb, const double *pos, const double *rad, double margin) {
+    cudaStream_t st = ctx->stream;
+    k_bounds<<<grid_for(nb), RELCP_NT, 0, st>>>(nb, pos, rad, ctx->partials.p, ctx->counter.p, ctx->red.p);
+    CKL();
+    CK(cudaMemcpyAsync(ctx->red_host, ctx->red.p, 7 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    double lo[3], hi[3], rmax = ctx->red_host[6];
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = ctx->red_host[k];
+        hi[k] = ctx->red_host[3 + k];
+    }
+    if (!(rmax > 0.0) || !isfinite(rmax)) return set_err(ctx, RELCP_E_ARG, "broadphase: bad radii / positions");
+    double csize = 2.0 * rmax + margin;
+    Grid G;
+    for (;;) {
+        double ncell = 1.0;
+        for (int k = 0; k < 3; ++k) {
+            G.box[k] = ctx->p.box[k];
+            if (G.box[k] > 0.0) {
+                int n = (int)floor(G.box[k] / csize);
+                G.nc[k] = n < 1 ? 1 : n;
+                G.lo[k] = 0.0;
+                G.cs[k] = G.box[k] / G.nc[k];
+            } else {
+                double ext = hi[k] - lo[k];
+                int n = (int)floor(ext / csize);
+                G.nc[k] = n < 1 ? 1 : n;
+                G.lo[k] = lo[k];
+                G.cs[k] = n < 1 ? fmax(ext, csize) : ext / n;
+                if (G.cs[k] < csize) G.cs[k] = csize;
+            }
+            ncell *= G.nc[k];
+        }
+        if (ncell <= 4.0 * (double)nb + 64.0) break;
+        csize *= 1.5;
+    }
+    const int64_t ncell = (int64_t)G.nc[0] * G.nc[1] * G.nc[2];
+    CK(ctx->cell_count.grow(ncell + 1));
+    CK(ctx->cell_start.grow(ncell + 1));
+    CK(ctx->cell_fill.grow(ncell + 1));
+    CK(ctx->cell_items.grow(nb));
+    CK(ctx->body_cell.grow(nb));
+    CK(ctx->pair_cnt.grow(nb + 1));
+    CK(cudaMemsetAsync(ctx->cell_count.p, 0, sizeof(int) * (ncell + 1), st));
+    CK(cudaMemsetAsync(ctx->cell_fill.p, 0, sizeof(int) * (ncell + 1), st));
+    k_cell_assign<<<grid_for(nb), RELCP_NT, 0, st>>>(nb, pos, G, ctx->body_cell.p, ctx->cell_count.p);
+    CKL();
+    CKS(scan_exclusive_int(ctx, ctx->cell_count.p, ctx->cell_start.p, ncell + 1, nullptr));
+    k_cell_fill<<<grid_for(nb), RELCP_NT, 0, st>>>(nb, ctx->body_cell.p, ctx->cell_start.p, ctx->cell_fill.p,
+                                                    ctx->cell_items.p);
+    CKL();
+    const int gp = grid_for(nb, 128, 32);
+    k_pairs2<0><<<gp, 128, 0, st>>>(nb, pos, rad, G, margin, ctx->body_cell.p, ctx->cell_start.p, ctx->cell_count.p,
+                                    ctx->cell_items.p, ctx->pair_cnt.p, nullptr, nullptr);
+    CKL();
+    CK(cudaMemsetAsync(ctx->pair_cnt.p + nb, 0, sizeof(long long), st));
+    long long total = 0;
+    CK(ctx->scan_ll.grow(nb + 1));
+    CKS(scan_exclusive_ll(ctx, ctx->pair_cnt.p, ctx->scan_ll.p, nb + 1, &total));
+    CK(ctx->pi.grow(total > 0 ? total : 1));
+    CK(ctx->pj.grow(total > 0 ? total : 1));
+    k_pairs2<1><<<gp, 128, 0, st>>>(nb, pos, rad, G, margin, ctx->body_cell.p, ctx->cell_start.p, ctx->cell_count.p,
+                                    ctx->cell_items.p, ctx->scan_ll.p, ctx->pi.p, ctx->pj.p);
+    CKL();
+    ctx->npairs = total;
+    return RELCP_OK;
+}

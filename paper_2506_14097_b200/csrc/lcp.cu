@@ -1,0 +1,220 @@
+// LCP solve 0 <= g = A x + q  _|_  x >= 0, A = s D^T W D (Lemma 3,
+// P:L280-299; CQP form P:L195-205) by Barzilai-Borwein projected gradient
+// (the paper names only the family; reading R1):
+//   alpha_0 = 1/L, L = ||A|| from power iterations;
+//   x+ = max(0, x - alpha g);  g+ = A x+ + q;  s = x+ - x;  y = g+ - g;
+//   alpha = s.s/s.y (BB1, even k) or s.y/y.y (BB2, odd k); 1/L if s.y <= 0;
+//   stop when r = ||min(x+, g+)||_inf <= tol (R2).
+//
+// One iteration = two streaming kernels:
+//   K6 scatter: U = W D max(0, x - alpha g)          (operator.cu, PROJ)
+//   K7 gather : x+, g+ = s D^T U + q, s.s, s.y, y.y, r partials; the last
+//               block finalizes alpha / convergence on the device.
+// Kernels early-exit once LcpState.done is set, so the host enqueues
+// `check_every` iterations blindly and reads the state once per batch.
+#include "common.cuh"
+#include "reduce.cuh"
+
+__device__ __forceinline__ double row_dot_l(int64_t a, int64_t cap, const int32_t *__restrict__ ia,
+                                            const int32_t *__restrict__ ib, const double *__restrict__ n,
+                                            const double *__restrict__ ta, const double *__restrict__ tb,
+                                            const double *__restrict__ U) {
+    const int i = ia[a], j = ib[a];
+    const double nx = n[a], ny = n[cap + a], nz = n[2 * cap + a];
+    const double *ua = U + 6 * (int64_t)i, *ub = U + 6 * (int64_t)j;
+    double v = nx * (ub[0] - ua[0]) + ny * (ub[1] - ua[1]) + nz * (ub[2] - ua[2]);
+    v -= ta[a] * ua[3] + ta[cap + a] * ua[4] + ta[2 * cap + a] * ua[5];
+    v += tb[a] * ub[3] + tb[cap + a] * ub[4] + tb[2 * cap + a] * ub[5];
+    return v;
+}
+
+__global__ void k_project(int64_t nc, double *x) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x)
+        x[a] = x[a] > 0.0 ? x[a] : 0.0;
+}
+
+__global__ void k_fill(int64_t n, double *v, double val) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n; a += (int64_t)gridDim.x * blockDim.x)
+        v[a] = val;
+}
+
+__global__ void k_state_init(LcpState *st, int64_t nc, double tol, long long max_iter) {
+    st->alpha = 0.0;
+    st->L = 0.0;
+    st->resid = 0.0;
+    st->ss = st->sy = st->yy = 0.0;
+    st->obj = 0.0;
+    st->pnorm = nc > 0 ? 1.0 / sqrt((double)nc) : 0.0;
+    st->tol = tol;
+    st->iter = 0;
+    st->max_iter = max_iter;
+    st->done = 0;
+    st->conv = 0;
+    st->nan = 0;
+}
+
+// g = s D^T U + q for the (projected) warm start; r_0; alpha_0 = 1/L.
+__global__ void __launch_bounds__(RELCP_NT) k_lcp_init(int64_t nc, int64_t cap, const int32_t *__restrict__ ia,
+                                                       const int32_t *__restrict__ ib, const double *__restrict__ n,
+                                                       const double *__restrict__ ta, const double *__restrict__ tb,
+                                                       const double *__restrict__ U, double s,
+                                                       const double *__restrict__ q, const double *__restrict__ x,
+                                                       double *__restrict__ g, double *part, unsigned *counter,
+                                                       LcpState *st) {
+    __shared__ double sh[64];
+    double acc[2] = {0.0, 0.0};
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
+        double gv = fma(s, row_dot_l(a, cap, ia, ib, n, ta, tb, U), q[a]);
+        g[a] = gv;
+        acc[0] = fmax(acc[0], fabs(fmin(x[a], gv)));
+        acc[1] = fmax(acc[1], isfinite(gv) ? 0.0 : 1.0);
+    }
+    const int ops[2] = {1, 1};
+    if (grid_reduce_last<2>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
+        double L = st->L > 0.0 && isfinite(st->L) ? st->L : 1.0;
+        st->L = L;
+        st->alpha = 1.0 / L;
+        st->resid = acc[0];
+        st->iter = 0;
+        if (acc[1] > 0.0) {
+            st->nan = 1;
+            st->done = 1;
+        } else if (acc[0] <= st->tol) {
+            st->conv = 1;
+            st->done = 1;
+        } else if (st->max_iter <= 0) {
+            st->done = 1;
+        }
+    }
+}
+
+// One BB projected-gradient update (the gather half of iteration k).
+__global__ void __launch_bounds__(RELCP_NT) k_lcp_iter(int64_t nc, int64_t cap, const int32_t *__restrict__ ia,
+                                                       const int32_t *__restrict__ ib, const double *__restrict__ n,
+                                                       const double *__restrict__ ta, const double *__restrict__ tb,
+                                                       const double *__restrict__ U, double s,
+                                                       const double *__restrict__ q, double *__restrict__ x,
+                                                       double *__restrict__ g, double *part, unsigned *counter,
+                                                       LcpState *st) {
+    __shared__ double sh[5 * 32];
+    if (st->done) return;
+    const double alpha = st->alpha;
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
+        const double xo = x[a], go = g[a];
+        const double xn = fmax(0.0, xo - alpha * go);
+        const double gn = fma(s, row_dot_l(a, cap, ia, ib, n, ta, tb, U), q[a]);
+        x[a] = xn;
+        g[a] = gn;
+        const double sd = xn - xo, yd = gn - go;
+        acc[0] = fma(sd, sd, acc[0]);
+        acc[1] = fma(sd, yd, acc[1]);
+        acc[2] = fma(yd, yd, acc[2]);
+        acc[3] = fmax(acc[3], fabs(fmin(xn, gn)));
+        acc[4] = fmax(acc[4], isfinite(gn) ? 0.0 : 1.0);
+    }
+    const int ops[5] = {0, 0, 0, 1, 1};
+    if (grid_reduce_last<5>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
+        const long long k = st->iter;
+        st->ss = acc[0];
+        st->sy = acc[1];
+        st->yy = acc[2];
+        st->resid = acc[3];
+        if (acc[4] > 0.0 || !isfinite(acc[0]) || !isfinite(acc[1]) || !isfinite(acc[2])) {
+            st->nan = 1;
+            st->done = 1;
+            st->iter = k + 1;
+            return;
+        }
+        if (acc[3] <= st->tol) {
+            st->conv = 1;
+            st->done = 1;
+            st->iter = k + 1;
+            return;
+        }
+        if (acc[1] <= 0.0 || acc[2] == 0.0)
+            st->alpha = 1.0 / st->L;
+        else
+            st->alpha = (k % 2 == 0) ? acc[0] / acc[1] : acc[1] / acc[2];
+        st->iter = k + 1;
+        if (k + 1 >= st->max_iter) st->done = 1;
+    }
+}
+
+// obj = x^T (g - q) = x^T A x
+__global__ void __launch_bounds__(RELCP_NT) k_objective(int64_t nc, const double *__restrict__ x,
+                                                        const double *__restrict__ g, const double *__restrict__ q,
+                                                        double *part, unsigned *counter, LcpState *st) {
+    __shared__ double sh[32];
+    double acc[1] = {0.0};
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x)
+        acc[0] = fma(x[a], g[a] - q[a], acc[0]);
+    const int ops[1] = {0};
+    if (grid_reduce_last<1>(acc, ops, part, counter, sh) && threadIdx.x == 0) st->obj = acc[0];
+}
+
+static double op_scale(const relcp_ctx *ctx) {
+    const double dt = ctx->p.dt;
+    return ctx->p.dynamics == RELCP_INERTIAL ? dt * dt : dt;  // P:L553 vs P:L512
+}
+
+int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relcp_solve_report *rep) {
+    const int64_t nc = cs->count, nb = b->n;
+    if (!cs->q || !cs->lambda || !cs->g) return set_err(ctx, RELCP_E_ARG, "solve: q, lambda and g are required");
+    if (ctx->op_nc != nc || ctx->op_nb != nb || ctx->op_key_ia != cs->ia) CKS(op_prepare(ctx, b, cs));
+    CK(ctx->vtmp.grow(nc > 0 ? nc : 1));
+    const double s = op_scale(ctx);
+    cudaStream_t st = ctx->stream;
+    k_state_init<<<1, 1, 0, st>>>(ctx->st.p, nc, ctx->p.lcp_tol, (long long)ctx->p.lcp_max_iter);
+    CKL();
+    if (nc == 0) {
+        if (rep) memset(rep, 0, sizeof(*rep));
+        if (rep) rep->converged = 1;
+        CK(cudaMemsetAsync(ctx->U.p, 0, sizeof(double) * 6 * nb, st));
+        CK(cudaStreamSynchronize(st));
+        return RELCP_OK;
+    }
+    const int gridc = grid_for(nc, RELCP_NT, 8);
+    k_project<<<gridc, RELCP_NT, 0, st>>>(nc, cs->lambda);
+    CKL();
+    // power iteration for L = ||A|| (alpha_0 = 1/L, R1)
+    k_fill<<<gridc, RELCP_NT, 0, st>>>(nc, ctx->vtmp.p, 1.0);
+    CKL();
+    for (int it = 0; it < ctx->p.power_iters; ++it) {
+        CKS(op_scatter(ctx, nb, ctx->vtmp.p, nullptr, 0, &ctx->st.p->pnorm, ctx->U.p, nullptr));
+        CKS(op_gather_apply(ctx, cs, ctx->U.p, ctx->vtmp.p, s, 1));
+    }
+    // g_0 = A x_0 + q
+    CKS(op_scatter(ctx, nb, cs->lambda, nullptr, 0, nullptr, ctx->U.p, nullptr));
+    k_lcp_init<<<gridc, RELCP_NT, 0, st>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->U.p, s, cs->q,
+                                           cs->lambda, cs->g, ctx->partials.p, ctx->counter.p, ctx->st.p);
+    CKL();
+    const int batch = ctx->p.check_every > 0 ? ctx->p.check_every : 32;
+    for (;;) {
+        CK(cudaMemcpyAsync(ctx->st_host, ctx->st.p, sizeof(LcpState), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (ctx->st_host->done) break;
+        for (int j = 0; j < batch; ++j) {
+            CKS(op_scatter(ctx, nb, cs->lambda, cs->g, 1, nullptr, ctx->U.p, nullptr));
+            k_lcp_iter<<<gridc, RELCP_NT, 0, st>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->U.p,
+                                                   s, cs->q, cs->lambda, cs->g, ctx->partials.p, ctx->counter.p,
+                                                   ctx->st.p);
+            CKL();
+        }
+    }
+    k_objective<<<gridc, RELCP_NT, 0, st>>>(nc, cs->lambda, cs->g, cs->q, ctx->partials.p, ctx->counter.p, ctx->st.p);
+    CKL();
+    CK(cudaMemcpyAsync(ctx->st_host, ctx->st.p, sizeof(LcpState), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const LcpState &h = *ctx->st_host;
+    if (rep) {
+        rep->iterations = h.iter;
+        rep->residual = h.resid;
+        rep->converged = h.conv;
+        rep->objective = -0.5 * h.obj;
+        rep->L = h.L;
+    }
+    if (h.nan) return set_err(ctx, RELCP_E_NAN, "solve: non-finite iterate after %lld iterations", h.iter);
+    if (!h.conv) return RELCP_W_MAX_ITER;
+    return RELCP_OK;
+}

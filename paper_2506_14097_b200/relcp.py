@@ -1,0 +1,322 @@
+"""Thin Python binding of librelcp.so (include/relcp.h).
+
+Argument marshalling only: every step of the ReLCP hot path runs in the CUDA
+kernels behind the C ABI.  torch is used for device memory and the stream.
+There is no CPU fallback: `Context` raises if the library or a CUDA device is
+missing.  Names follow the ABI (relcp_generate_contacts -> generate_contacts).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+from . import build as _build
+
+INERTIAL = 0
+OVERDAMPED = 1
+MAX_REC = 64
+
+OK = 0
+E_ARG, E_CUDA, E_CAPACITY, E_DEGENERATE, E_NAN, E_STATE = -1, -2, -3, -4, -5, -6
+W_MAX_ITER, W_RECURSION_CAP, W_SNSD_NONCONV = 1, 2, 3
+
+EXPORTS = ["relcp_default_params", "relcp_create", "relcp_destroy", "relcp_last_error", "relcp_set_params",
+           "relcp_generate_contacts", "relcp_prepare_operator", "relcp_delassus_apply", "relcp_wrench",
+           "relcp_solve_lcp", "relcp_check_and_augment", "relcp_step", "relcp_get_pairs", "relcp_snsd_pairs"]
+
+P = ctypes.c_void_p
+i32, i64, f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("dynamics", i32), ("max_recursions", i32), ("dt", f64), ("eps_ncp", f64), ("cutoff", f64),
+                ("lcp_tol", f64), ("lcp_max_iter", i64), ("check_every", i32), ("power_iters", i32),
+                ("box", f64 * 3), ("xi", f64), ("n_dirs", i32), ("reserved", i32)]
+
+
+class Bodies(ctypes.Structure):
+    _fields_ = [("n", i64), ("pos", P), ("quat", P), ("axes", P), ("vel", P), ("inv_mass", P),
+                ("inv_inertia", P), ("kinematic", P)]
+
+
+class Constraints(ctypes.Structure):
+    _fields_ = [("capacity", i64), ("count", i64), ("ia", P), ("ib", P), ("gen", P), ("n", P), ("ta", P),
+                ("tb", P), ("phi", P), ("q", P), ("lam", P), ("g", P)]
+
+
+class SolveReport(ctypes.Structure):
+    _fields_ = [("iterations", i64), ("residual", f64), ("converged", i32), ("pad", i32), ("objective", f64),
+                ("L", f64)]
+
+
+class StepReport(ctypes.Structure):
+    _fields_ = [("recursions", i32), ("status", i32), ("n_pairs", i64), ("margin", f64), ("max_overlap", f64),
+                ("n_c", i64 * MAX_REC), ("lcp_iters", i64 * MAX_REC), ("residual", f64 * MAX_REC),
+                ("f_n", f64 * MAX_REC), ("ms_generate", f64), ("ms_solve", f64), ("ms_check", f64),
+                ("snsd_nonconv", i64)]
+
+    def as_dict(self):
+        r = self.recursions
+        return dict(recursions=r, status=self.status, n_pairs=self.n_pairs, margin=self.margin,
+                    max_overlap=self.max_overlap, n_c=list(self.n_c[:r + 1]),
+                    iterations=list(self.lcp_iters[:r + 1]), residuals=list(self.residual[:r + 1]),
+                    f=list(self.f_n[:r + 1]), ms_generate=self.ms_generate, ms_solve=self.ms_solve,
+                    ms_check=self.ms_check, snsd_nonconv=self.snsd_nonconv)
+
+
+_lib = None
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = True):
+    """Load librelcp.so (building it if absent); raises if it cannot."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.LIB
+    if not os.path.exists(path):
+        if not build_if_missing:
+            raise RuntimeError(f"librelcp.so missing at {path}; run paper_2506_14097_b200.build")
+        _build.build()
+    L = ctypes.CDLL(path)
+    L.relcp_default_params.argtypes = [ctypes.POINTER(Params)]
+    L.relcp_default_params.restype = None
+    L.relcp_create.argtypes = [ctypes.POINTER(P), ctypes.POINTER(Params), P]
+    L.relcp_destroy.argtypes = [P]
+    L.relcp_last_error.argtypes = [P]
+    L.relcp_last_error.restype = ctypes.c_char_p
+    L.relcp_set_params.argtypes = [P, ctypes.POINTER(Params)]
+    L.relcp_generate_contacts.argtypes = [P, ctypes.POINTER(Bodies), ctypes.POINTER(Constraints),
+                                          ctypes.POINTER(i64)]
+    L.relcp_prepare_operator.argtypes = [P, ctypes.POINTER(Bodies), ctypes.POINTER(Constraints)]
+    L.relcp_delassus_apply.argtypes = [P, ctypes.POINTER(Bodies), ctypes.POINTER(Constraints), P, P, f64]
+    L.relcp_wrench.argtypes = [P, ctypes.POINTER(Bodies), ctypes.POINTER(Constraints), P, P, P]
+    L.relcp_solve_lcp.argtypes = [P, ctypes.POINTER(Bodies), ctypes.POINTER(Constraints),
+                                  ctypes.POINTER(SolveReport)]
+    L.relcp_check_and_augment.argtypes = [P, ctypes.POINTER(Bodies), ctypes.POINTER(Constraints), i32,
+                                          ctypes.POINTER(i64), ctypes.POINTER(f64)]
+    L.relcp_step.argtypes = [P, ctypes.POINTER(Bodies), P, ctypes.POINTER(Constraints), ctypes.POINTER(StepReport)]
+    L.relcp_get_pairs.argtypes = [P, P, P, i64, ctypes.POINTER(i64)]
+    L.relcp_snsd_pairs.argtypes = [P, ctypes.POINTER(Bodies), i64, P, P, P, P, P, P, P]
+    for name in EXPORTS:
+        if name not in ("relcp_default_params", "relcp_last_error"):
+            getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+class RelcpError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"relcp error {code}: {msg}")
+        self.code = code
+
+
+def default_params(**kw) -> Params:
+    p = Params()
+    load().relcp_default_params(ctypes.byref(p))
+    for k, v in kw.items():
+        if k == "box":
+            for i in range(3):
+                p.box[i] = float(v[i])
+        else:
+            setattr(p, k, v)
+    return p
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+class BodyState:
+    """Device-resident SoA body arrays (fp64; kinematic int32)."""
+
+    def __init__(self, pos, quat, axes, vel=None, inv_mass=None, inv_inertia=None, kinematic=None,
+                 device="cuda"):
+        def t(a, dt=torch.float64):
+            if a is None:
+                return None
+            return torch.as_tensor(np.ascontiguousarray(a) if isinstance(a, np.ndarray) else a, dtype=dt,
+                                   device=device).contiguous()
+        self.pos, self.quat, self.axes = t(pos), t(quat), t(axes)
+        self.vel, self.inv_mass, self.inv_inertia = t(vel), t(inv_mass), t(inv_inertia)
+        self.kinematic = t(kinematic, torch.int32)
+        self.n = self.pos.shape[0]
+
+    @classmethod
+    def from_scene(cls, sc, device="cuda"):
+        return cls(sc["pos"], sc["quat"], sc["axes"], sc.get("vel"), sc.get("inv_mass"), sc.get("inv_inertia"),
+                   sc.get("kinematic"), device=device)
+
+    def view(self) -> Bodies:
+        return Bodies(self.n, _ptr(self.pos), _ptr(self.quat), _ptr(self.axes), _ptr(self.vel), _ptr(self.inv_mass),
+                      _ptr(self.inv_inertia), _ptr(self.kinematic))
+
+
+class ConstraintStore:
+    """Caller-owned SoA constraint store (include/relcp.h relcp_constraints)."""
+
+    def __init__(self, capacity: int, device="cuda"):
+        cap = max(int(capacity), 1)
+        self.capacity = cap
+        self.count = 0
+        z32 = lambda: torch.zeros(cap, dtype=torch.int32, device=device)
+        z64 = lambda *s: torch.zeros(*s, dtype=torch.float64, device=device)
+        self.ia, self.ib, self.gen = z32(), z32(), z32()
+        self.n, self.ta, self.tb = z64(3, cap), z64(3, cap), z64(3, cap)
+        self.phi, self.q, self.lam, self.g = z64(cap), z64(cap), z64(cap), z64(cap)
+        self._view = None
+
+    @classmethod
+    def from_rows(cls, ia, ib, nrm, ta, tb, q=None, lam=None, capacity=None, device="cuda"):
+        m = len(ia)
+        cs = cls(capacity or m, device)
+        cs.count = m
+        if m:
+            cs.ia[:m] = torch.as_tensor(np.asarray(ia), dtype=torch.int32)
+            cs.ib[:m] = torch.as_tensor(np.asarray(ib), dtype=torch.int32)
+            cs.n[:, :m] = torch.as_tensor(np.asarray(nrm, dtype=np.float64).T)
+            cs.ta[:, :m] = torch.as_tensor(np.asarray(ta, dtype=np.float64).T)
+            cs.tb[:, :m] = torch.as_tensor(np.asarray(tb, dtype=np.float64).T)
+            if q is not None:
+                cs.q[:m] = torch.as_tensor(np.asarray(q, dtype=np.float64))
+            if lam is not None:
+                cs.lam[:m] = torch.as_tensor(np.asarray(lam, dtype=np.float64))
+        return cs
+
+    def view(self) -> Constraints:
+        v = Constraints(self.capacity, self.count, _ptr(self.ia), _ptr(self.ib), _ptr(self.gen), _ptr(self.n),
+                        _ptr(self.ta), _ptr(self.tb), _ptr(self.phi), _ptr(self.q), _ptr(self.lam), _ptr(self.g))
+        self._view = v
+        return v
+
+    def sync_from(self, v: Constraints):
+        self.count = int(v.count)
+
+    def to_numpy(self):
+        m = self.count
+        c = lambda t: t[..., :m].cpu().numpy()
+        return dict(ia=c(self.ia), ib=c(self.ib), gen=c(self.gen), n=c(self.n).T.copy(), ta=c(self.ta).T.copy(),
+                    tb=c(self.tb).T.copy(), phi=c(self.phi), q=c(self.q), lam=c(self.lam), g=c(self.g))
+
+
+class Context:
+    """relcp_ctx bound to a torch CUDA stream."""
+
+    def __init__(self, params: Params | None = None, stream: torch.cuda.Stream | None = None, **kw):
+        if not torch.cuda.is_available():
+            raise RuntimeError("relcp: no CUDA device (there is no CPU fallback)")
+        self.L = load()
+        self.params = params if params is not None else default_params(**kw)
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        h = P()
+        rc = self.L.relcp_create(ctypes.byref(h), ctypes.byref(self.params), P(self.stream.cuda_stream))
+        if rc != OK:
+            raise RelcpError(rc, "relcp_create failed")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.relcp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc, allow_warn=True):
+        if rc < 0 or (rc > 0 and not allow_warn):
+            raise RelcpError(rc, self.L.relcp_last_error(self.h).decode(errors="replace"))
+        return rc
+
+    def set_params(self, **kw):
+        for k, v in kw.items():
+            if k == "box":
+                for i in range(3):
+                    self.params.box[i] = float(v[i])
+            else:
+                setattr(self.params, k, v)
+        self._check(self.L.relcp_set_params(self.h, ctypes.byref(self.params)))
+
+    # ---- ABI calls
+    def generate_contacts(self, bodies: BodyState, cs: ConstraintStore):
+        bv, cv = bodies.view(), cs.view()
+        n = i64()
+        rc = self.L.relcp_generate_contacts(self.h, ctypes.byref(bv), ctypes.byref(cv), ctypes.byref(n))
+        cs.sync_from(cv)
+        self._check(rc)
+        return int(n.value), rc
+
+    def prepare_operator(self, bodies: BodyState, cs: ConstraintStore):
+        bv, cv = bodies.view(), cs.view()
+        self._check(self.L.relcp_prepare_operator(self.h, ctypes.byref(bv), ctypes.byref(cv)))
+        self._op = (bv, cv)
+
+    def delassus_apply(self, bodies: BodyState, cs: ConstraintStore, x: torch.Tensor, y: torch.Tensor,
+                       scale: float = 1.0):
+        bv, cv = bodies.view(), cs.view()
+        self._check(self.L.relcp_delassus_apply(self.h, ctypes.byref(bv), ctypes.byref(cv), _ptr(x), _ptr(y),
+                                                float(scale)))
+
+    def wrench(self, bodies: BodyState, cs: ConstraintStore, x: torch.Tensor, F=None, U=None):
+        bv, cv = bodies.view(), cs.view()
+        self._check(self.L.relcp_wrench(self.h, ctypes.byref(bv), ctypes.byref(cv), _ptr(x), _ptr(F), _ptr(U)))
+
+    def solve_lcp(self, bodies: BodyState, cs: ConstraintStore):
+        bv, cv = bodies.view(), cs.view()
+        rep = SolveReport()
+        rc = self.L.relcp_solve_lcp(self.h, ctypes.byref(bv), ctypes.byref(cv), ctypes.byref(rep))
+        self._check(rc)
+        return dict(iterations=rep.iterations, residual=rep.residual, converged=bool(rep.converged),
+                    objective=rep.objective, L=rep.L, status=rc)
+
+    def check_and_augment(self, bodies: BodyState, cs: ConstraintStore, recursion: int):
+        bv, cv = bodies.view(), cs.view()
+        n = i64()
+        mp = f64()
+        rc = self.L.relcp_check_and_augment(self.h, ctypes.byref(bv), ctypes.byref(cv), int(recursion),
+                                            ctypes.byref(n), ctypes.byref(mp))
+        cs.sync_from(cv)
+        self._check(rc)
+        return int(n.value), float(mp.value)
+
+    def step(self, bodies: BodyState, cs: ConstraintStore, f_ext: torch.Tensor | None = None):
+        bv, cv = bodies.view(), cs.view()
+        rep = StepReport()
+        rc = self.L.relcp_step(self.h, ctypes.byref(bv), _ptr(f_ext), ctypes.byref(cv), ctypes.byref(rep))
+        cs.sync_from(cv)
+        self._check(rc)
+        d = rep.as_dict()
+        d["rc"] = rc
+        return d
+
+    def get_pairs(self):
+        n = i64()
+        self._check(self.L.relcp_get_pairs(self.h, None, None, 0, ctypes.byref(n)))
+        m = int(n.value)
+        pi = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
+        pj = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
+        self._check(self.L.relcp_get_pairs(self.h, _ptr(pi), _ptr(pj), m, ctypes.byref(n)))
+        return pi[:m], pj[:m]
+
+    def snsd_pairs(self, bodies: BodyState, pi, pj):
+        pi = torch.as_tensor(np.asarray(pi), dtype=torch.int32, device="cuda") if not torch.is_tensor(pi) else pi
+        pj = torch.as_tensor(np.asarray(pj), dtype=torch.int32, device="cuda") if not torch.is_tensor(pj) else pj
+        m = pi.numel()
+        phi = torch.empty(max(m, 1), dtype=torch.float64, device="cuda")
+        nrm = torch.empty(3, max(m, 1), dtype=torch.float64, device="cuda")
+        ra = torch.empty_like(nrm)
+        rb = torch.empty_like(nrm)
+        st = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
+        bv = bodies.view()
+        self._check(self.L.relcp_snsd_pairs(self.h, ctypes.byref(bv), m, _ptr(pi), _ptr(pj), _ptr(phi), _ptr(nrm),
+                                            _ptr(ra), _ptr(rb), _ptr(st)))
+        torch.cuda.synchronize()
+        return phi[:m], nrm[:, :m], ra[:, :m], rb[:, :m], st[:m]

@@ -1,0 +1,324 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on
+the same seeded inputs (gen/scenes.py).  Tolerances (BASELINE north_star,
+SURVEY §8(c)):
+  * constraint pair lists / indices: bit-exact (outside the guard band R14);
+  * Delassus apply: ||y - y_ref||_inf <= 1e-12 ||y_ref||_inf;
+  * SNSD: Phi 1e-12 max(1, |d|) abs, n 1e-10;
+  * LCP: lambda 1e-6 relative (where unique, R13), D lambda and g 1e-6
+    relative, GPU residual < tol;
+  * trial / accepted configurations 1e-9 abs.
+"""
+import numpy as np
+import pytest
+
+from gen import scenes
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def R():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test collected without a CUDA device")
+    from paper_2506_14097_b200 import relcp
+    relcp.load()
+    return relcp
+
+
+def _ctx(R, sc, **kw):
+    p = dict(dynamics=sc["dynamics"], dt=sc["dt"], cutoff=sc["cutoff"], eps_ncp=sc["eps_ncp"],
+             box=list(sc["box"]), xi=sc.get("xi", 1.0))
+    p.update(kw)
+    return R.Context(**p)
+
+
+def _net(orc, nb, nc, seed, dynamics):
+    b, ia, ib, n, ra, rb = scenes.random_constraint_network(nb, nc, seed, dynamics)
+    ta, tb = np.cross(ra, n), np.cross(rb, n)
+    return b, ia, ib, n, ta, tb
+
+
+# ------------------------------------------------------------ Delassus apply
+
+@pytest.mark.parametrize("dynamics", [0, 1])
+@pytest.mark.parametrize("nb,nc", [(7, 1), (97, 1000), (2000, 9973), (5000, 40001)])
+def test_delassus_apply_parity(orc, R, dynamics, nb, nc):
+    b, ia, ib, n, ta, tb = _net(orc, nb, nc, 11 + nb, dynamics)
+    b["dynamics"] = dynamics
+    W = orc.body_W(b)
+    rng = np.random.default_rng(nb)
+    x = rng.standard_normal(nc)
+    s = 0.37
+    y_ref = orc.delassus_apply(W, ia, ib, n, ta, tb, s, x)
+    ctx = _ctx(R, dict(dynamics=dynamics, dt=1e-3, cutoff=0.1, eps_ncp=1e-5, box=[0, 0, 0]))
+    bodies = R.BodyState.from_scene(b)
+    cs = R.ConstraintStore.from_rows(ia, ib, n, ta, tb, capacity=nc + 13)
+    ctx.prepare_operator(bodies, cs)
+    xd = torch.as_tensor(x, device="cuda")
+    yd = torch.empty_like(xd)
+    ctx.delassus_apply(bodies, cs, xd, yd, s)
+    y = yd.cpu().numpy()
+    assert np.max(np.abs(y - y_ref)) <= 1e-12 * np.max(np.abs(y_ref))
+    # determinism: bitwise identical on repeat
+    yd2 = torch.empty_like(xd)
+    ctx.delassus_apply(bodies, cs, xd, yd2, s)
+    assert torch.equal(yd, yd2)
+    # wrench F = D x and U = W D x
+    F_ref, U_ref = orc.wrench(W, ia, ib, n, ta, tb, x)
+    F = torch.empty(nb, 6, dtype=torch.float64, device="cuda")
+    U = torch.empty_like(F)
+    ctx.wrench(bodies, cs, xd, F, U)
+    assert np.max(np.abs(F.cpu().numpy() - F_ref)) <= 1e-12 * np.max(np.abs(F_ref))
+    assert np.max(np.abs(U.cpu().numpy() - U_ref)) <= 1e-12 * np.max(np.abs(U_ref))
+
+
+def test_delassus_empty_and_state(orc, R):
+    b, ia, ib, n, ta, tb = _net(orc, 10, 5, 3, 0)
+    ctx = _ctx(R, dict(dynamics=0, dt=1e-3, cutoff=0.1, eps_ncp=1e-5, box=[0, 0, 0]))
+    bodies = R.BodyState.from_scene(b)
+    cs = R.ConstraintStore.from_rows(ia, ib, n, ta, tb)
+    x = torch.ones(5, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(x)
+    with pytest.raises(R.RelcpError) as e:  # operator not prepared
+        ctx.delassus_apply(bodies, cs, x, y)
+    assert e.value.code == R.E_STATE
+    empty = R.ConstraintStore(4)
+    ctx.prepare_operator(bodies, empty)
+    ctx.delassus_apply(bodies, empty, x, y)  # no-op
+    bad = R.ConstraintStore.from_rows([3], [3], n[:1], ta[:1], tb[:1])
+    with pytest.raises(R.RelcpError):
+        ctx.prepare_operator(bodies, bad)
+
+
+# ------------------------------------------------------------ LCP
+
+@pytest.fixture(scope="module")
+def cfg1_a0(orc):
+    sc = scenes.cfg1()
+    r = orc.relcp_step(sc, snsd_only=True, lcp_tol=1e-10)
+    return sc, r
+
+
+def test_lcp_solve_parity_cfg1(orc, R, cfg1_a0):
+    sc, r = cfg1_a0
+    c = r["constraints"]
+    ctx = _ctx(R, sc, lcp_tol=1e-10)
+    bodies = R.BodyState.from_scene(sc)
+    cs = R.ConstraintStore.from_rows(c["ia"], c["ib"], c["n"], c["ta"], c["tb"], q=r["q_hist"][0])
+    rep = ctx.solve_lcp(bodies, cs)
+    assert rep["converged"] and rep["residual"] <= 1e-10
+    lam = cs.lam[:cs.count].cpu().numpy()
+    g = cs.g[:cs.count].cpu().numpy()
+    lam_ref, g_ref = c["lam"], r["g_hist"][0]
+    assert np.all(lam >= 0)
+    assert np.max(np.abs(lam - lam_ref)) <= 1e-6 * np.max(np.abs(lam_ref))
+    assert np.max(np.abs(g - g_ref)) <= 1e-6 * max(1e-300, np.max(np.abs(g_ref))) + 1e-9
+    # D lambda (unique by Lemma 5)
+    W = r["W"]
+    F_ref, _ = orc.wrench(W, c["ia"], c["ib"], c["n"], c["ta"], c["tb"], lam_ref)
+    F = torch.empty(sc["n"], 6, dtype=torch.float64, device="cuda")
+    ctx.prepare_operator(bodies, cs)
+    ctx.wrench(bodies, cs, cs.lam[:cs.count].contiguous(), F, None)
+    assert np.max(np.abs(F.cpu().numpy() - F_ref)) <= 1e-6 * np.max(np.abs(F_ref))
+    # objective f = -1/2 lambda^T A lambda
+    assert abs(rep["objective"] - r["f"][0]) <= 1e-6 * abs(r["f"][0])
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_lcp_vs_enumeration_tiny(orc, R, seed):
+    """Tiny random LCPs: the GPU solution equals the brute-force support
+    enumeration."""
+    b, ia, ib, n, ta, tb = _net(orc, 6, 9, 100 + seed, 0)
+    b["dynamics"] = 0
+    W = orc.body_W(b)
+    nc = len(ia)
+    A = np.stack([orc.delassus_apply(W, ia, ib, n, ta, tb, 1.0, e) for e in np.eye(nc)], 1)
+    q = np.random.default_rng(seed).standard_normal(nc)
+    x_ref = orc.enumerate_lcp(A, q)
+    ctx = _ctx(R, dict(dynamics=0, dt=1.0, cutoff=0.1, eps_ncp=1e-5, box=[0, 0, 0]), lcp_tol=1e-12)
+    bodies = R.BodyState.from_scene(b)
+    cs = R.ConstraintStore.from_rows(ia, ib, n, ta, tb, q=q)
+    rep = ctx.solve_lcp(bodies, cs)
+    assert rep["converged"]
+    x = cs.lam[:nc].cpu().numpy()
+    # compare the unique image A x (Lemma 5) and x itself when A is nonsingular
+    assert np.max(np.abs(A @ x - A @ x_ref)) <= 1e-9 * (1 + np.max(np.abs(q)))
+    if np.linalg.matrix_rank(A) == nc:
+        assert np.max(np.abs(x - x_ref)) <= 1e-6 * max(1.0, np.max(np.abs(x_ref)))
+
+
+def test_lcp_warm_start_and_zero(orc, R):
+    """q >= 0 -> lambda = 0; warm start from the solution converges at once."""
+    b, ia, ib, n, ta, tb = _net(orc, 50, 120, 5, 0)
+    ctx = _ctx(R, dict(dynamics=0, dt=1.0, cutoff=0.1, eps_ncp=1e-5, box=[0, 0, 0]), lcp_tol=1e-12)
+    bodies = R.BodyState.from_scene(b)
+    cs = R.ConstraintStore.from_rows(ia, ib, n, ta, tb, q=np.abs(np.random.default_rng(1).standard_normal(120)))
+    rep = ctx.solve_lcp(bodies, cs)
+    assert rep["converged"] and rep["iterations"] == 0
+    assert torch.count_nonzero(cs.lam[:120]).item() == 0
+    cs.q[:120] = torch.as_tensor(np.random.default_rng(2).standard_normal(120), device="cuda")
+    rep = ctx.solve_lcp(bodies, cs)
+    assert rep["converged"]
+    rep2 = ctx.solve_lcp(bodies, cs)
+    assert rep2["converged"] and rep2["iterations"] <= 1
+
+
+# ------------------------------------------------------------ SNSD + broadphase
+
+def test_snsd_parity_cfg1_pairs(orc, R, cfg1_a0):
+    sc, r = cfg1_a0
+    pi, pj = r["pairs"]
+    phi_r, n_r, ra_r, rb_r, st_r = orc.snsd(sc["pos"], sc["quat"], sc["axes"], sc["box"], pi, pj)
+    ctx = _ctx(R, sc)
+    bodies = R.BodyState.from_scene(sc)
+    phi, n, ra, rb, st = ctx.snsd_pairs(bodies, pi, pj)
+    phi, n, ra, rb, st = (t.cpu().numpy() for t in (phi, n, ra, rb, st))
+    assert np.all(st == 0) and np.all(st_r == 0)
+    d = sc["pos"][pj] - sc["pos"][pi]
+    d -= sc["box"] * np.rint(d / sc["box"])
+    dn = np.linalg.norm(d, axis=1)
+    assert np.all(np.abs(phi - phi_r) <= 1e-12 * np.maximum(1, dn))
+    assert np.max(np.abs(n.T - n_r)) <= 1e-10
+    assert np.max(np.abs(ra.T - ra_r)) <= 1e-9 and np.max(np.abs(rb.T - rb_r)) <= 1e-9
+
+
+def test_snsd_random_overlaps(orc, R):
+    """Deep overlaps of elongated pairs (cfg2 shapes), the multistart branch."""
+    rng = np.random.default_rng(7)
+    m = 3000
+    pos = np.zeros((2 * m, 3))
+    pos[1::2] = rng.uniform(-1.2, 1.2, size=(m, 3))
+    quat = rng.standard_normal((2 * m, 4))
+    quat /= np.linalg.norm(quat, axis=1, keepdims=True)
+    r = rng.uniform(1, 4, size=2 * m)
+    axes = np.stack([np.ones(2 * m), 1 / r, 1 / r], 1)
+    pi = np.arange(0, 2 * m, 2, dtype=np.int32)
+    pj = pi + 1
+    phi_r, n_r, *_ = orc.snsd(pos, quat, axes, None, pi, pj)
+    ctx = R.Context(dynamics=1, dt=1e-2)
+    bodies = R.BodyState(pos, quat, axes)
+    phi, n, ra, rb, st = ctx.snsd_pairs(bodies, pi, pj)
+    phi = phi.cpu().numpy()
+    dn = np.linalg.norm(pos[pj] - pos[pi], axis=1)
+    err = np.abs(phi - phi_r) / np.maximum(1, dn)
+    assert np.sum(phi_r < 0) > 500
+    assert np.max(err) <= 1e-12, (np.argmax(err), phi[np.argmax(err)], phi_r[np.argmax(err)])
+
+
+@pytest.mark.parametrize("n,phi_v", [(512, 0.3), (4000, 0.55), (20000, 0.55)])
+def test_broadphase_parity(orc, R, n, phi_v):
+    sc = scenes.suspension(n, (1.0, 0.6, 0.4), phi_v, 3)
+    ctx = _ctx(R, sc)
+    bodies = R.BodyState.from_scene(sc)
+    cs = R.ConstraintStore(20 * n)
+    ctx.generate_contacts(bodies, cs)
+    pi, pj = ctx.get_pairs()
+    ri, rj = orc.broadphase(sc["pos"], sc["axes"].max(1), sc["box"], sc["cutoff"])
+    assert np.array_equal(pi.cpu().numpy(), ri) and np.array_equal(pj.cpu().numpy(), rj)
+
+
+def test_broadphase_open_planar(orc, R):
+    """Non-periodic planar layout (cfg3-like disk in z = 0)."""
+    rng = np.random.default_rng(3)
+    n = 3000
+    ang = rng.uniform(0, 2 * np.pi, n)
+    rr = 30 * np.sqrt(rng.uniform(0, 1, n))
+    pos = np.stack([rr * np.cos(ang), rr * np.sin(ang), np.zeros(n)], 1)
+    axes = np.stack([rng.uniform(0.5, 1.0, n), np.full(n, 0.25), np.full(n, 0.25)], 1)
+    quat = np.zeros((n, 4))
+    th = rng.uniform(0, np.pi, n)
+    quat[:, 0], quat[:, 3] = np.cos(th / 2), np.sin(th / 2)
+    ctx = R.Context(dynamics=1, dt=1e-2)
+    bodies = R.BodyState(pos, quat, axes)
+    cs = R.ConstraintStore(20 * n)
+    ctx.generate_contacts(bodies, cs)
+    pi, pj = ctx.get_pairs()
+    ri, rj = orc.broadphase(pos, axes.max(1), None, 0.1, "brute")
+    assert np.array_equal(pi.cpu().numpy(), ri) and np.array_equal(pj.cpu().numpy(), rj)
+
+
+def test_generate_contacts_parity_cfg1(orc, R, cfg1_a0):
+    sc, r = cfg1_a0
+    c = r["constraints"]
+    ctx = _ctx(R, sc)
+    bodies = R.BodyState.from_scene(sc)
+    cs = R.ConstraintStore(4 * len(c["ia"]))
+    n0, rc = ctx.generate_contacts(bodies, cs)
+    g = cs.to_numpy()
+    assert n0 == len(c["ia"])
+    assert np.array_equal(g["ia"], c["ia"]) and np.array_equal(g["ib"], c["ib"])
+    assert np.all(g["gen"] == 0)
+    assert np.max(np.abs(g["phi"] - c["phi"])) <= 1e-12 * 10
+    assert np.max(np.abs(g["n"] - c["n"])) <= 1e-10
+    assert np.max(np.abs(g["ta"] - c["ta"])) <= 1e-9 and np.max(np.abs(g["tb"] - c["tb"])) <= 1e-9
+    assert np.max(np.abs(g["q"] - r["q_hist"][0])) <= 1e-11
+    # capacity error reports the required size and writes nothing
+    small = R.ConstraintStore(3)
+    with pytest.raises(R.RelcpError) as e:
+        ctx.generate_contacts(bodies, small)
+    assert e.value.code == R.E_CAPACITY and small.count == n0
+
+
+# ------------------------------------------------------------ full step
+
+def _sorted_rows(ia, ib, gen):
+    return np.lexsort((ib, ia, gen))
+
+
+def _compare_step(orc, R, sc, tol_cfg=1e-9, **kw):
+    r = orc.relcp_step(sc, lcp_tol=1e-10, **kw)
+    ctx = _ctx(R, sc, lcp_tol=1e-10)
+    bodies = R.BodyState.from_scene(sc)
+    cs = R.ConstraintStore(8 * max(1, len(r["constraints"]["ia"])) + 64)
+    rep = ctx.step(bodies, cs)
+    assert rep["recursions"] == r["recursions"]
+    assert rep["n_c"] == r["n_c"]
+    g = cs.to_numpy()
+    c = r["constraints"]
+    og, oo = _sorted_rows(g["ia"], g["ib"], g["gen"]), _sorted_rows(c["ia"], c["ib"], c["gen"])
+    assert np.array_equal(g["ia"][og], c["ia"][oo]) and np.array_equal(g["ib"][og], c["ib"][oo])
+    assert np.array_equal(g["gen"][og], c["gen"][oo])
+    assert np.max(np.abs(g["n"][og] - c["n"][oo])) <= 1e-8
+    pos = bodies.pos.cpu().numpy()
+    dpos = pos - r["pos"]
+    if np.all(sc["box"] > 0):
+        dpos -= sc["box"] * np.rint(dpos / sc["box"])
+    assert np.max(np.abs(dpos)) <= tol_cfg
+    assert np.max(np.abs(bodies.quat.cpu().numpy() - r["quat"])) <= tol_cfg
+    if bodies.vel is not None:
+        v_ref = r["vel"]
+        assert np.max(np.abs(bodies.vel.cpu().numpy() - v_ref)) <= 1e-6 * max(1.0, np.max(np.abs(v_ref)))
+    assert rep["max_overlap"] <= sc["eps_ncp"] or rep["status"] != 0
+    # f_n non-increasing (Thm 1 proof)
+    f = np.array(rep["f"])
+    assert np.all(np.diff(f) <= 1e-6 * np.max(np.abs(f)) + 1e-12)
+    return r, rep, g
+
+
+def test_step_parity_cfg1(orc, R):
+    _compare_step(orc, R, scenes.cfg1())
+
+
+def test_step_parity_overdamped_small(orc, R):
+    sc = scenes.cfg2(n=1500)
+    _compare_step(orc, R, sc)
+
+
+def test_step_parity_bigdt_augments(orc, R):
+    sc = scenes.suspension(300, (1.0, 0.6, 0.4), 0.3, 9, dt=2e-2)
+    r, rep, _ = _compare_step(orc, R, sc)
+    assert rep["recursions"] >= 1
+
+
+def test_step_deterministic(R):
+    sc = scenes.cfg1()
+    out = []
+    for _ in range(2):
+        ctx = _ctx(R, sc)
+        bodies = R.BodyState.from_scene(sc)
+        cs = R.ConstraintStore(8000)
+        ctx.step(bodies, cs)
+        out.append((bodies.pos.clone(), bodies.vel.clone(), cs.lam[:cs.count].clone()))
+    assert all(torch.equal(a, b) for a, b in zip(out[0], out[1]))
