@@ -232,6 +232,23 @@ int relcp_step(relcp_ctx *ctx, relcp_bodies *inout, const double *f_ext, relcp_c
  * pairs in (i, j) lexicographic order.  Synchronises. */
 int relcp_get_pairs(relcp_ctx *ctx, int32_t *pi, int32_t *pj, int64_t cap, int64_t *n_pairs);
 
+/* Counters kept by the context since creation / the last reset:
+ *   launches          kernels this context launched (all entry points)
+ *   lcp_iterations    BB iterations executed (K6 scatter + K7 gather pairs)
+ * and, when timing is on (relcp_set_timing(ctx, 1)), CUDA-event durations on
+ * the context stream of every executed LCP iteration:
+ *   scatter_ms / gather_ms  summed K6 / K7 durations, iter_timed = count. */
+typedef struct relcp_stats {
+    int64_t launches;
+    int64_t lcp_iterations;
+    int64_t iter_timed;
+    double scatter_ms;
+    double gather_ms;
+} relcp_stats;
+int relcp_get_stats(relcp_ctx *ctx, relcp_stats *out);
+int relcp_reset_stats(relcp_ctx *ctx);
+int relcp_set_timing(relcp_ctx *ctx, int32_t on);
+
 /* SNSD of explicit pairs (device arrays, length n_pairs) at the given bodies:
  * phi (P), nrm (3,P) planes, ra (3,P), rb (3,P) planes (r = y - x), status
  * (P) int32 0 ok / 1 coincident centres / 2 not certified.  Asynchronous. */

@@ -391,6 +391,8 @@ int relcp_destroy(relcp_ctx *ctx) {
     ctx->tflag.release(); ctx->tstat.release(); ctx->scan_ll.release(); ctx->scan_tmp.release();
     ctx->cell_count.release(); ctx->cell_start.release(); ctx->cell_fill.release(); ctx->cell_items.release();
     ctx->body_cell.release(); ctx->pair_cnt.release(); ctx->red.release();
+    if (ctx->ev_ready)
+        for (int k = 0; k < 3 * 64; ++k) cudaEventDestroy(ctx->ev[k]);
     if (ctx->st_host) cudaFreeHost(ctx->st_host);
     if (ctx->red_host) cudaFreeHost(ctx->red_host);
     delete ctx;
@@ -540,6 +542,31 @@ int relcp_step(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_const
     if (rep) *rep = R;
     if (R.status) return R.status;
     return warn > 0 ? warn : RELCP_OK;
+}
+
+int relcp_get_stats(relcp_ctx *ctx, relcp_stats *out) {
+    if (!ctx || !out) return RELCP_E_ARG;
+    out->launches = ctx->launches;
+    out->lcp_iterations = ctx->lcp_iterations;
+    out->iter_timed = ctx->iter_timed;
+    out->scatter_ms = ctx->scatter_ms;
+    out->gather_ms = ctx->gather_ms;
+    return RELCP_OK;
+}
+
+int relcp_reset_stats(relcp_ctx *ctx) {
+    if (!ctx) return RELCP_E_ARG;
+    ctx->launches = 0;
+    ctx->lcp_iterations = 0;
+    ctx->iter_timed = 0;
+    ctx->scatter_ms = ctx->gather_ms = 0.0;
+    return RELCP_OK;
+}
+
+int relcp_set_timing(relcp_ctx *ctx, int32_t on) {
+    if (!ctx) return RELCP_E_ARG;
+    ctx->timing = on != 0;
+    return RELCP_OK;
 }
 
 int relcp_get_pairs(relcp_ctx *ctx, int32_t *pi, int32_t *pj, int64_t cap, int64_t *n_pairs) {

@@ -102,6 +102,15 @@ struct relcp_ctx {
     DevBuf<double> red;          // small reduction buffer
     double *red_host = nullptr;  // pinned (64 doubles)
     int64_t snsd_nonconv_total = 0;
+
+    // counters / timing (relcp_get_stats)
+    int64_t launches = 0;
+    int64_t lcp_iterations = 0;
+    int timing = 0;
+    int64_t iter_timed = 0;
+    double scatter_ms = 0.0, gather_ms = 0.0;
+    cudaEvent_t ev[3 * 64] = {};
+    int ev_ready = 0;
 };
 
 // ------------------------------------------------------------ error helpers
@@ -117,6 +126,7 @@ int set_err(relcp_ctx *c, int code, const char *fmt, ...);
 
 #define CKL()                                                                      \
     do {                                                                           \
+        ++ctx->launches;                                                           \
         cudaError_t e_ = cudaGetLastError();                                       \
         if (e_ != cudaSuccess)                                                     \
             return set_err(ctx, RELCP_E_CUDA, "%s:%d launch: %s", __FILE__, __LINE__, \

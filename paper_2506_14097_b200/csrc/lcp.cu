@@ -189,18 +189,44 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
     k_lcp_init<<<gridc, RELCP_NT, 0, st>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->U.p, s, cs->q,
                                            cs->lambda, cs->g, ctx->partials.p, ctx->counter.p, ctx->st.p);
     CKL();
-    const int batch = ctx->p.check_every > 0 ? ctx->p.check_every : 32;
+    int batch = ctx->p.check_every > 0 ? ctx->p.check_every : 32;
+    if (ctx->timing) {
+        if (batch > 64) batch = 64;
+        if (!ctx->ev_ready) {
+            for (int k = 0; k < 3 * 64; ++k) CK(cudaEventCreate(&ctx->ev[k]));
+            ctx->ev_ready = 1;
+        }
+    }
+    long long it_before = 0;
+    int pending = 0;
     for (;;) {
         CK(cudaMemcpyAsync(ctx->st_host, ctx->st.p, sizeof(LcpState), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        const long long executed = ctx->st_host->iter - it_before;
+        ctx->lcp_iterations += executed;
+        if (ctx->timing && pending > 0) {
+            for (long long j = 0; j < executed && j < pending; ++j) {
+                float a = 0.f, b2 = 0.f;
+                CK(cudaEventElapsedTime(&a, ctx->ev[3 * j], ctx->ev[3 * j + 1]));
+                CK(cudaEventElapsedTime(&b2, ctx->ev[3 * j + 1], ctx->ev[3 * j + 2]));
+                ctx->scatter_ms += a;
+                ctx->gather_ms += b2;
+                ++ctx->iter_timed;
+            }
+        }
+        it_before = ctx->st_host->iter;
         if (ctx->st_host->done) break;
         for (int j = 0; j < batch; ++j) {
+            if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j], st));
             CKS(op_scatter(ctx, nb, cs->lambda, cs->g, 1, nullptr, ctx->U.p, nullptr));
+            if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j + 1], st));
             k_lcp_iter<<<gridc, RELCP_NT, 0, st>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->U.p,
                                                    s, cs->q, cs->lambda, cs->g, ctx->partials.p, ctx->counter.p,
                                                    ctx->st.p);
             CKL();
+            if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j + 2], st));
         }
+        pending = batch;
     }
     k_objective<<<gridc, RELCP_NT, 0, st>>>(nc, cs->lambda, cs->g, cs->q, ctx->partials.p, ctx->counter.p, ctx->st.p);
     CKL();

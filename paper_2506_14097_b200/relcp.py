@@ -25,7 +25,8 @@ W_MAX_ITER, W_RECURSION_CAP, W_SNSD_NONCONV = 1, 2, 3
 
 EXPORTS = ["relcp_default_params", "relcp_create", "relcp_destroy", "relcp_last_error", "relcp_set_params",
            "relcp_generate_contacts", "relcp_prepare_operator", "relcp_delassus_apply", "relcp_wrench",
-           "relcp_solve_lcp", "relcp_check_and_augment", "relcp_step", "relcp_get_pairs", "relcp_snsd_pairs"]
+           "relcp_solve_lcp", "relcp_check_and_augment", "relcp_step", "relcp_get_pairs", "relcp_snsd_pairs",
+           "relcp_get_stats", "relcp_reset_stats", "relcp_set_timing"]
 
 P = ctypes.c_void_p
 i32, i64, f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
@@ -50,6 +51,11 @@ class Constraints(ctypes.Structure):
 class SolveReport(ctypes.Structure):
     _fields_ = [("iterations", i64), ("residual", f64), ("converged", i32), ("pad", i32), ("objective", f64),
                 ("L", f64)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("launches", i64), ("lcp_iterations", i64), ("iter_timed", i64), ("scatter_ms", f64),
+                ("gather_ms", f64)]
 
 
 class StepReport(ctypes.Structure):
@@ -104,6 +110,9 @@ def load(build_if_missing: bool = True):
     L.relcp_step.argtypes = [P, ctypes.POINTER(Bodies), P, ctypes.POINTER(Constraints), ctypes.POINTER(StepReport)]
     L.relcp_get_pairs.argtypes = [P, P, P, i64, ctypes.POINTER(i64)]
     L.relcp_snsd_pairs.argtypes = [P, ctypes.POINTER(Bodies), i64, P, P, P, P, P, P, P]
+    L.relcp_get_stats.argtypes = [P, ctypes.POINTER(Stats)]
+    L.relcp_reset_stats.argtypes = [P]
+    L.relcp_set_timing.argtypes = [P, i32]
     for name in EXPORTS:
         if name not in ("relcp_default_params", "relcp_last_error"):
             getattr(L, name).restype = ctypes.c_int
@@ -296,6 +305,18 @@ class Context:
         d = rep.as_dict()
         d["rc"] = rc
         return d
+
+    def stats(self):
+        st = Stats()
+        self._check(self.L.relcp_get_stats(self.h, ctypes.byref(st)))
+        return dict(launches=st.launches, lcp_iterations=st.lcp_iterations, iter_timed=st.iter_timed,
+                    scatter_ms=st.scatter_ms, gather_ms=st.gather_ms)
+
+    def reset_stats(self):
+        self._check(self.L.relcp_reset_stats(self.h))
+
+    def set_timing(self, on: bool):
+        self._check(self.L.relcp_set_timing(self.h, 1 if on else 0))
 
     def get_pairs(self):
         n = i64()

@@ -267,13 +267,14 @@ def _sorted_rows(ia, ib, gen):
     return np.lexsort((ib, ia, gen))
 
 
-def _compare_step(orc, R, sc, tol_cfg=1e-9, **kw):
-    r = orc.relcp_step(sc, lcp_tol=1e-10, **kw)
-    ctx = _ctx(R, sc, lcp_tol=1e-10)
+def _compare_step(orc, R, sc, tol_cfg=1e-9, max_recursions=50):
+    r = orc.relcp_step(sc, lcp_tol=1e-10, max_recursions=max_recursions)
+    ctx = _ctx(R, sc, lcp_tol=1e-10, max_recursions=max_recursions, lcp_max_iter=2_000_000)
     bodies = R.BodyState.from_scene(sc)
     cs = R.ConstraintStore(8 * max(1, len(r["constraints"]["ia"])) + 64)
     rep = ctx.step(bodies, cs)
     assert rep["recursions"] == r["recursions"]
+    assert (rep["status"] != 0) == (r["status"] != 0)
     assert rep["n_c"] == r["n_c"]
     g = cs.to_numpy()
     c = r["constraints"]
@@ -301,15 +302,24 @@ def test_step_parity_cfg1(orc, R):
     _compare_step(orc, R, scenes.cfg1())
 
 
-def test_step_parity_overdamped_small(orc, R):
-    sc = scenes.cfg2(n=1500)
-    _compare_step(orc, R, sc)
+def test_step_parity_overdamped_cfg2_recipe(orc, R):
+    """cfg2 recipe (overdamped local drag, R12) at 400 bodies, recursion cap 1."""
+    sc = scenes.cfg2(n=400)
+    r, rep, _ = _compare_step(orc, R, sc, max_recursions=1)
+    assert rep["status"] == R.W_RECURSION_CAP
 
 
 def test_step_parity_bigdt_augments(orc, R):
     sc = scenes.suspension(300, (1.0, 0.6, 0.4), 0.3, 9, dt=2e-2)
-    r, rep, _ = _compare_step(orc, R, sc)
+    r, rep, _ = _compare_step(orc, R, sc, max_recursions=2)
     assert rep["recursions"] >= 1
+
+
+def test_step_parity_cfg5_recipe(orc, R):
+    """cfg5 recipe (the bench workload) at 1000 bodies, two augmentations."""
+    sc = scenes.cfg5(n=1000)
+    r, rep, _ = _compare_step(orc, R, sc, max_recursions=2)
+    assert rep["recursions"] == 2
 
 
 def test_step_deterministic(R):

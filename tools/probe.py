@@ -10,9 +10,9 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 2_000_000
 t0 = time.time()
 sc = scenes.cfg5(n=n)
 print("gen", time.time() - t0, flush=True)
-ctx = R.Context(dynamics=sc["dynamics"], dt=sc["dt"], box=list(sc["box"]), lcp_max_iter=int(sys.argv[2]) if len(sys.argv) > 2 else 20000)
+ctx = R.Context(dynamics=sc["dynamics"], dt=sc["dt"], box=list(sc["box"]), lcp_max_iter=int(sys.argv[2]) if len(sys.argv) > 2 else 20000, max_recursions=int(sys.argv[3]) if len(sys.argv) > 3 else 2)
 bodies = R.BodyState.from_scene(sc)
-cs = R.ConstraintStore(8 * n)
+cs = R.ConstraintStore(24 * n)
 torch.cuda.synchronize()
 t = time.time(); n0, rc = ctx.generate_contacts(bodies, cs); torch.cuda.synchronize()
 print("generate", time.time() - t, "n0", n0, "pairs", ctx.get_pairs()[0].numel(), "rc", rc, flush=True)
