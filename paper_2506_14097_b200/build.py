@@ -36,16 +36,20 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile every csrc/*.cu into one shared library (default: LIB).
+    `defines` / `out` build tuning variants (e.g. SCATTER_MINB=6) side by side."""
+    target = out or LIB
+    if not force and out is None and not defines and not stale():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
-    cmd = [NVCC, *ARCH, *FLAGS, *(["-Xptxas", "-v"] if ptxas_v else []), "-o", LIB + ".tmp", *sources()]
+    os.makedirs(os.path.dirname(target), exist_ok=True)
+    cmd = [NVCC, *ARCH, *FLAGS, *(["-Xptxas", "-v"] if ptxas_v else []), *("-D" + d for d in defines),
+           "-o", target + ".tmp", *sources()]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

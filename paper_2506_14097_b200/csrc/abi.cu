@@ -43,7 +43,8 @@ __global__ void k_ufree(int64_t nb, int dyn, double dt, const double *__restrict
                         const double *__restrict__ fext, const double *__restrict__ W,
                         const int32_t *__restrict__ kin, double *__restrict__ uf) {
     for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
-        const double *w = W + RELCP_WSTRIDE * b;
+        double w[7];
+        for (int k = 0; k < 7; ++k) w[k] = W[k * nb + b];  // SoA planes
         double f[6] = {0, 0, 0, 0, 0, 0};
         if (fext)
             for (int k = 0; k < 6; ++k) f[k] = fext[6 * b + k];

@@ -52,11 +52,12 @@ struct LcpState {
     int pad;
 };
 
-// Per-body mobility block W_b in a single 7-double form:
+// Per-body mobility block W_b in a single 7-double form, stored as 7 SoA
+// planes W[k * nb + b]:
 //   U_lin = w[0] * F_lin ;  U_ang = S F_ang, S symmetric = {w1..w6} =
 //   (xx, xy, xz, yy, yz, zz).  Inertial: w0 = 1/m, S = R I^-1 R^T;
 //   overdamped local drag: w0 = 1/(xi L), S = 12/(xi L^3) I.
-#define RELCP_WSTRIDE 8
+#define RELCP_WSTRIDE 7
 
 struct relcp_ctx {
     relcp_params p;

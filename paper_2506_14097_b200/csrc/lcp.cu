@@ -15,18 +15,11 @@
 #include "common.cuh"
 #include "reduce.cuh"
 
-__device__ __forceinline__ double row_dot_l(int64_t a, int64_t cap, const int32_t *__restrict__ ia,
-                                            const int32_t *__restrict__ ib, const double *__restrict__ n,
-                                            const double *__restrict__ ta, const double *__restrict__ tb,
-                                            const double *__restrict__ U) {
-    const int i = ia[a], j = ib[a];
-    const double nx = n[a], ny = n[cap + a], nz = n[2 * cap + a];
-    const double *ua = U + 6 * (int64_t)i, *ub = U + 6 * (int64_t)j;
-    double v = nx * (ub[0] - ua[0]) + ny * (ub[1] - ua[1]) + nz * (ub[2] - ua[2]);
-    v -= ta[a] * ua[3] + ta[cap + a] * ua[4] + ta[2 * cap + a] * ua[5];
-    v += tb[a] * ub[3] + tb[cap + a] * ub[4] + tb[2 * cap + a] * ub[5];
-    return v;
-}
+#include "rows.cuh"
+#define row_dot_l row_dot_u
+#ifndef ITER_MINB
+#define ITER_MINB 4  // resident K7 blocks per SM (register budget); grid = 148 * ITER_MINB
+#endif
 
 __global__ void k_project(int64_t nc, double *x) {
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x)
@@ -89,7 +82,7 @@ __global__ void __launch_bounds__(RELCP_NT) k_lcp_init(int64_t nc, int64_t cap, 
 }
 
 // One BB projected-gradient update (the gather half of iteration k).
-__global__ void __launch_bounds__(RELCP_NT) k_lcp_iter(int64_t nc, int64_t cap, const int32_t *__restrict__ ia,
+__global__ void __launch_bounds__(RELCP_NT, ITER_MINB) k_lcp_iter(int64_t nc, int64_t cap, const int32_t *__restrict__ ia,
                                                        const int32_t *__restrict__ ib, const double *__restrict__ n,
                                                        const double *__restrict__ ta, const double *__restrict__ tb,
                                                        const double *__restrict__ U, double s,
@@ -100,18 +93,35 @@ __global__ void __launch_bounds__(RELCP_NT) k_lcp_iter(int64_t nc, int64_t cap, 
     if (st->done) return;
     const double alpha = st->alpha;
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
-        const double xo = x[a], go = g[a];
-        const double xn = fmax(0.0, xo - alpha * go);
-        const double gn = fma(s, row_dot_l(a, cap, ia, ib, n, ta, tb, U), q[a]);
-        x[a] = xn;
-        g[a] = gn;
-        const double sd = xn - xo, yd = gn - go;
-        acc[0] = fma(sd, sd, acc[0]);
-        acc[1] = fma(sd, yd, acc[1]);
-        acc[2] = fma(yd, yd, acc[2]);
-        acc[3] = fmax(acc[3], fabs(fmin(xn, gn)));
-        acc[4] = fmax(acc[4], isfinite(gn) ? 0.0 : 1.0);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // two constraints per thread per trip: independent loads in flight (ILP)
+    for (int64_t a0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a0 < nc; a0 += 2 * stride) {
+        double xo[2], go[2], qv[2], rd[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t a = a0 + u * stride;
+            const bool ok = a < nc;
+            const int64_t ac = ok ? a : a0;
+            xo[u] = x[ac];
+            go[u] = g[ac];
+            qv[u] = q[ac];
+            rd[u] = row_dot_l(ac, cap, ia, ib, n, ta, tb, U);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t a = a0 + u * stride;
+            if (a >= nc) continue;
+            const double xn = fmax(0.0, xo[u] - alpha * go[u]);
+            const double gn = fma(s, rd[u], qv[u]);
+            x[a] = xn;
+            g[a] = gn;
+            const double sd = xn - xo[u], yd = gn - go[u];
+            acc[0] = fma(sd, sd, acc[0]);
+            acc[1] = fma(sd, yd, acc[1]);
+            acc[2] = fma(yd, yd, acc[2]);
+            acc[3] = fmax(acc[3], fabs(fmin(xn, gn)));
+            acc[4] = fmax(acc[4], isfinite(gn) ? 0.0 : 1.0);
+        }
     }
     const int ops[5] = {0, 0, 0, 1, 1};
     if (grid_reduce_last<5>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
@@ -174,7 +184,7 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
         CK(cudaStreamSynchronize(st));
         return RELCP_OK;
     }
-    const int gridc = grid_for(nc, RELCP_NT, 8);
+    const int gridc = grid_for(nc, RELCP_NT, ITER_MINB);  // one wave of resident blocks
     k_project<<<gridc, RELCP_NT, 0, st>>>(nc, cs->lambda);
     CKL();
     // power iteration for L = ||A|| (alpha_0 = 1/L, R1)

@@ -7,17 +7,28 @@
 //   W_b = M_b^{-1} or local-drag mobility
 //
 // B200 layout:
-//   * scatter F = D x is a body-major CSR pass: each body owns a contiguous
-//     segment of signed 6-double wrench payloads (built once per operator,
-//     sorted by (constraint, side) so the per-body sum has a fixed order);
-//     a G-lane group of one warp reduces a body's segment with shuffles, then
-//     six lanes apply W_b and store U_b.  No floating-point atomics.
-//   * gather y = s D^T U is a constraint-major streaming pass over the SoA
-//     store (coalesced n / t_a / t_b planes) with U_a, U_b read from L2.
+//   * scatter U = W D x (K6) is a body-major CSR pass.  Each body owns a
+//     contiguous segment of signed 6-double wrench payloads, built once per
+//     operator and ordered (side, constraint): the a-side entries of a store
+//     sorted by (ia, ib) come first and reference consecutive constraints, so
+//     their x / g loads arrive in contiguous runs.  One warp owns 32 bodies
+//     (one per lane); the warp's entries are streamed in coalesced 64-entry
+//     tiles into shared memory and each lane sums its own body's entries in
+//     segment order (fixed association: bitwise deterministic, no atomics),
+//     then applies W_b (SoA planes, coalesced) and stores U_b through a
+//     shared-memory transpose (coalesced).
+//   * gather y = s D^T U (K7) is a constraint-major streaming pass over the
+//     SoA store (coalesced n / t_a / t_b planes) with U_a, U_b read from L2.
 #include "common.cuh"
 #include "reduce.cuh"
 
-// ------------------------------------------------------------ W blocks
+#define SCATTER_WPB 8    // warps per block
+#define SCATTER_TILE 64  // entries staged per warp per tile
+#ifndef SCATTER_MINB
+#define SCATTER_MINB 6   // resident blocks per SM the register budget must allow (sweep: 6 best)
+#endif
+
+// ------------------------------------------------------------ W blocks (SoA planes)
 __global__ void k_build_W(int64_t nb, int dyn, double xi, const double *__restrict__ quat,
                           const double *__restrict__ axes, const double *__restrict__ inv_mass,
                           const double *__restrict__ inv_inertia, const int32_t *__restrict__ kin,
@@ -44,8 +55,7 @@ __global__ void k_build_W(int64_t nb, int dyn, double xi, const double *__restri
         }
         bool k = kin && kin[b] != 0;
 #pragma unroll
-        for (int i = 0; i < 7; ++i) W[RELCP_WSTRIDE * b + i] = k ? 0.0 : w[i];
-        W[RELCP_WSTRIDE * b + 7] = 0.0;
+        for (int i = 0; i < 7; ++i) W[i * nb + b] = k ? 0.0 : w[i];  // SoA planes
     }
 }
 
@@ -71,18 +81,20 @@ __global__ void k_degree(int64_t nc, const int32_t *__restrict__ ia, const int32
     }
 }
 
+// entry key = side << 30 | constraint (side 0 = a, 1 = b); nc < 2^30
+#define EKEY_SIDE (1 << 30)
 __global__ void k_fill_slots(int64_t nc, const int32_t *__restrict__ ia, const int32_t *__restrict__ ib,
                              const int *__restrict__ row_ptr, int *fill, int *ekey) {
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
         int i = ia[a], j = ib[a];
         int si = row_ptr[i] + atomicAdd(fill + i, 1);
         int sj = row_ptr[j] + atomicAdd(fill + j, 1);
-        ekey[si] = (int)(2 * a);      // side a
-        ekey[sj] = (int)(2 * a + 1);  // side b
+        ekey[si] = (int)a;              // side a
+        ekey[sj] = (int)a | EKEY_SIDE;  // side b
     }
 }
 
-// Sort each body segment by key (constraint, side): fixes the summation order.
+// Sort each body segment by key (side, constraint): fixes the summation order.
 __global__ void k_sort_segments(int64_t nb, const int *__restrict__ row_ptr, int *ekey) {
     for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
         int s = row_ptr[b], e = row_ptr[b + 1];
@@ -98,10 +110,10 @@ __global__ void k_sort_segments(int64_t nb, const int *__restrict__ row_ptr, int
 __global__ void k_payload(int64_t E, int64_t cap, const double *__restrict__ n, const double *__restrict__ ta,
                           const double *__restrict__ tb, int *ekey, double *__restrict__ ew) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
-        int key = ekey[e];
-        int64_t a = key >> 1;
-        bool side_b = key & 1;
-        double sg = side_b ? 1.0 : -1.0;
+        const int key = ekey[e];
+        const int64_t a = key & (EKEY_SIDE - 1);
+        const bool side_b = (key & EKEY_SIDE) != 0;
+        const double sg = side_b ? 1.0 : -1.0;
         const double *t = side_b ? tb : ta;
         ew[0 * E + e] = sg * n[a];
         ew[1 * E + e] = sg * n[cap + a];
@@ -155,132 +167,119 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
     return RELCP_OK;
 }
 
-// ------------------------------------------------------------ scatter
+// ------------------------------------------------------------ scatter (K6)
 // U_b = W_b sum_{e in seg(b)} w_e * xeff(cid_e), xeff = proj ? max(0, x - alpha g) : x,
-// scaled by *xscale if given.  G lanes per body.
-template <int G, bool PROJ>
-__global__ void __launch_bounds__(RELCP_NT) k_scatter(int64_t nb, int64_t E, const int *__restrict__ row_ptr,
-                                                      const int *__restrict__ ecid, const double *__restrict__ ew,
-                                                      const double *__restrict__ x, const double *__restrict__ g,
-                                                      const LcpState *__restrict__ st,
-                                                      const double *__restrict__ xscale,
-                                                      const double *__restrict__ W, double *__restrict__ U,
-                                                      double *__restrict__ Fout) {
-    constexpr int BPW = 32 / G;
+// scaled by *xscale if given; optionally F_b = the raw sum.
+template <bool PROJ>
+__global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
+    int64_t nb, int64_t E, const int *__restrict__ row_ptr, const int *__restrict__ ecid,
+    const double *__restrict__ ew, const double *__restrict__ x, const double *__restrict__ g,
+    const LcpState *__restrict__ st, const double *__restrict__ xscale, const double *__restrict__ W,
+    double *__restrict__ U, double *__restrict__ Fout) {
+    // contributions staged as 3 planes of double2 (components 01, 23, 45):
+    // 128-bit shared loads in the per-lane segment sums
+    __shared__ double2 sm[SCATTER_WPB][3][SCATTER_TILE + 1];
     double alpha = 0.0;
     if (PROJ) {
         if (st->done) return;
         alpha = st->alpha;
     }
     const double sc = xscale ? *xscale : 1.0;
-    const int lane = threadIdx.x & 31, lg = lane % G, grp = lane / G;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t base = warp * BPW; base < nb; base += nwarp * BPW) {
-        const int64_t b = base + grp;
-        const bool valid = b < nb;
-        double f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0, f5 = 0;
-        if (valid) {
-            const int s = row_ptr[b], e1 = row_ptr[b + 1];
-            for (int e = s + lg; e < e1; e += G) {
-                const int c = ecid[e];
-                double xv = x[c];
-                if (PROJ) xv = fmax(0.0, xv - alpha * g[c]);
-                xv *= sc;
-                f0 = fma(ew[e], xv, f0);
-                f1 = fma(ew[E + e], xv, f1);
-                f2 = fma(ew[2 * E + e], xv, f2);
-                f3 = fma(ew[3 * E + e], xv, f3);
-                f4 = fma(ew[4 * E + e], xv, f4);
-                f5 = fma(ew[5 * E + e], xv, f5);
-            }
-        }
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    double2(*c6)[SCATTER_TILE + 1] = sm[wl];
+    const int64_t nwarp = (nb + 31) >> 5;
+    for (int64_t w = blockIdx.x * (int64_t)SCATTER_WPB + wl; w < nwarp; w += (int64_t)gridDim.x * SCATTER_WPB) {
+        const int64_t b0 = w << 5;
+        const int64_t b = b0 + lane;
+        const bool own = b < nb;
+        const int s = own ? row_ptr[b] : 0, t = own ? row_ptr[b + 1] : 0;
+        const int e0 = __shfl_sync(0xffffffffu, s, 0);
+        const int last = nb - b0 < 32 ? (int)(nb - b0 - 1) : 31;
+        const int e1 = __shfl_sync(0xffffffffu, t, last);
+        double f[6] = {0, 0, 0, 0, 0, 0};
+        for (int base = e0; base < e1; base += SCATTER_TILE) {
+            // stage the tile's contributions (coalesced loads)
 #pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) {
-            f0 += __shfl_down_sync(0xffffffffu, f0, o, G);
-            f1 += __shfl_down_sync(0xffffffffu, f1, o, G);
-            f2 += __shfl_down_sync(0xffffffffu, f2, o, G);
-            f3 += __shfl_down_sync(0xffffffffu, f3, o, G);
-            f4 += __shfl_down_sync(0xffffffffu, f4, o, G);
-            f5 += __shfl_down_sync(0xffffffffu, f5, o, G);
-        }
-        // broadcast the group's lane-0 totals (one association for all lanes)
-        const int src = grp * G;
-        f0 = __shfl_sync(0xffffffffu, f0, src);
-        f1 = __shfl_sync(0xffffffffu, f1, src);
-        f2 = __shfl_sync(0xffffffffu, f2, src);
-        f3 = __shfl_sync(0xffffffffu, f3, src);
-        f4 = __shfl_sync(0xffffffffu, f4, src);
-        f5 = __shfl_sync(0xffffffffu, f5, src);
-        if (valid && lg < 6) {
-            const double *w = W + RELCP_WSTRIDE * b;
-            double u;
-            if (lg < 3) {
-                u = w[0] * (lg == 0 ? f0 : (lg == 1 ? f1 : f2));
-            } else if (lg == 3) {
-                u = w[1] * f3 + w[2] * f4 + w[3] * f5;
-            } else if (lg == 4) {
-                u = w[2] * f3 + w[4] * f4 + w[5] * f5;
-            } else {
-                u = w[3] * f3 + w[5] * f4 + w[6] * f5;
+            for (int i = 0; i < SCATTER_TILE / 32; ++i) {
+                const int e = base + lane + 32 * i;
+                double v[6] = {0, 0, 0, 0, 0, 0};
+                if (e < e1) {
+                    const int c = ecid[e];
+                    double xv = x[c];
+                    if (PROJ) xv = fmax(0.0, xv - alpha * g[c]);
+                    xv *= sc;
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) v[k] = ew[k * E + e] * xv;
+                }
+#pragma unroll
+                for (int k = 0; k < 3; ++k) c6[k][lane + 32 * i] = make_double2(v[2 * k], v[2 * k + 1]);
             }
-            U[6 * b + lg] = u;
-            if (Fout) {
-                double fv = lg == 0 ? f0 : lg == 1 ? f1 : lg == 2 ? f2 : lg == 3 ? f3 : lg == 4 ? f4 : f5;
-                Fout[6 * b + lg] = fv;
+            __syncwarp();
+            // each lane sums its own body's entries inside the tile, in order
+            const int lo = max(s, base) - base, hi = min(t, base + SCATTER_TILE) - base;
+            for (int j = lo; j < hi; ++j)
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const double2 c = c6[k][j];
+                    f[2 * k] += c.x;
+                    f[2 * k + 1] += c.y;
+                }
+            __syncwarp();
+        }
+        // U_b = W_b F_b ; staged through shared memory for a coalesced AoS store
+        double u[6] = {0, 0, 0, 0, 0, 0};
+        if (own) {
+            const double w0 = W[b], s00 = W[nb + b], s01 = W[2 * nb + b], s02 = W[3 * nb + b], s11 = W[4 * nb + b],
+                         s12 = W[5 * nb + b], s22 = W[6 * nb + b];
+            u[0] = w0 * f[0];
+            u[1] = w0 * f[1];
+            u[2] = w0 * f[2];
+            u[3] = s00 * f[3] + s01 * f[4] + s02 * f[5];
+            u[4] = s01 * f[3] + s11 * f[4] + s12 * f[5];
+            u[5] = s02 * f[3] + s12 * f[4] + s22 * f[5];
+        }
+        double *flat = &c6[0][0].x;  // 3 * 65 double2 >= 2 * 192 doubles
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            flat[6 * lane + k] = u[k];
+            flat[192 + 6 * lane + k] = f[k];
+        }
+        __syncwarp();
+        const int64_t nvals = 6 * (int64_t)(last + 1);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            const int m = lane + 32 * i;
+            if (m < nvals) {
+                U[6 * b0 + m] = flat[m];
+                if (Fout) Fout[6 * b0 + m] = flat[192 + m];
             }
         }
+        __syncwarp();
     }
-}
-
-static int scatter_group(const relcp_ctx *ctx) {
-    // mean half-entries per body decides the group width
-    double mean = ctx->op_nb > 0 ? 2.0 * (double)ctx->op_nc / (double)ctx->op_nb : 0.0;
-    return mean > 24.0 ? 32 : (mean > 10.0 ? 16 : 8);
-}
-
-template <bool PROJ>
-static void launch_scatter(relcp_ctx *ctx, int G, int64_t nb, const double *x, const double *g,
-                           const double *xscale, double *U, double *F) {
-    const int64_t E = 2 * ctx->op_nc;
-    int64_t threads = nb * G;
-    int grid = grid_for(threads, RELCP_NT, 16);
-    const LcpState *st = ctx->st.p;
-    if (G == 8)
-        k_scatter<8, PROJ><<<grid, RELCP_NT, 0, ctx->stream>>>(nb, E, ctx->row_ptr.p, ctx->ecid.p, ctx->ew.p, x, g, st,
-                                                              xscale, ctx->W.p, U, F);
-    else if (G == 16)
-        k_scatter<16, PROJ><<<grid, RELCP_NT, 0, ctx->stream>>>(nb, E, ctx->row_ptr.p, ctx->ecid.p, ctx->ew.p, x, g, st,
-                                                               xscale, ctx->W.p, U, F);
-    else
-        k_scatter<32, PROJ><<<grid, RELCP_NT, 0, ctx->stream>>>(nb, E, ctx->row_ptr.p, ctx->ecid.p, ctx->ew.p, x, g, st,
-                                                               xscale, ctx->W.p, U, F);
 }
 
 int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int proj, const double *xscale_dev,
                double *U, double *F) {
-    int G = scatter_group(ctx);
+    const int64_t E = 2 * ctx->op_nc;
+    const int64_t nwarp = (nb + 31) / 32;
+    int64_t grid = (nwarp + SCATTER_WPB - 1) / SCATTER_WPB;
+    if (grid > (int64_t)RELCP_SM_COUNT * 64) grid = (int64_t)RELCP_SM_COUNT * 64;
+    if (grid < 1) grid = 1;
     if (proj)
-        launch_scatter<true>(ctx, G, nb, x, g, xscale_dev, U, F);
+        k_scatter<true><<<(unsigned)grid, 32 * SCATTER_WPB, 0, ctx->stream>>>(nb, E, ctx->row_ptr.p, ctx->ecid.p,
+                                                                              ctx->ew.p, x, g, ctx->st.p, xscale_dev,
+                                                                              ctx->W.p, U, F);
     else
-        launch_scatter<false>(ctx, G, nb, x, g, xscale_dev, U, F);
+        k_scatter<false><<<(unsigned)grid, 32 * SCATTER_WPB, 0, ctx->stream>>>(nb, E, ctx->row_ptr.p, ctx->ecid.p,
+                                                                               ctx->ew.p, x, g, ctx->st.p, xscale_dev,
+                                                                               ctx->W.p, U, F);
     CKL();
     return RELCP_OK;
 }
 
 // ------------------------------------------------------------ gather
-__device__ __forceinline__ double row_dot(int64_t a, int64_t cap, const int32_t *__restrict__ ia,
-                                          const int32_t *__restrict__ ib, const double *__restrict__ n,
-                                          const double *__restrict__ ta, const double *__restrict__ tb,
-                                          const double *__restrict__ U) {
-    const int i = ia[a], j = ib[a];
-    const double nx = n[a], ny = n[cap + a], nz = n[2 * cap + a];
-    const double *ua = U + 6 * (int64_t)i, *ub = U + 6 * (int64_t)j;
-    double v = nx * (ub[0] - ua[0]) + ny * (ub[1] - ua[1]) + nz * (ub[2] - ua[2]);
-    v -= ta[a] * ua[3] + ta[cap + a] * ua[4] + ta[2 * cap + a] * ua[5];
-    v += tb[a] * ub[3] + tb[cap + a] * ub[4] + tb[2 * cap + a] * ub[5];
-    return v;
-}
+#include "rows.cuh"
+#define row_dot row_dot_u
 
 // y = scale * D^T U ; optionally the grid-wide ||y||^2 -> st->pnorm = 1/||y||, st->L = ||y||
 __global__ void __launch_bounds__(RELCP_NT) k_gather(int64_t nc, int64_t cap, const int32_t *__restrict__ ia,
@@ -291,10 +290,21 @@ __global__ void __launch_bounds__(RELCP_NT) k_gather(int64_t nc, int64_t cap, co
                                                      unsigned *counter, LcpState *st) {
     __shared__ double sh[32];
     double acc[1] = {0.0};
-    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
-        double v = scale * row_dot(a, cap, ia, ib, n, ta, tb, U);
-        y[a] = v;
-        acc[0] = fma(v, v, acc[0]);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t a0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a0 < nc; a0 += 2 * stride) {
+        double v[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t a = a0 + u * stride;
+            v[u] = scale * row_dot(a < nc ? a : a0, cap, ia, ib, n, ta, tb, U);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t a = a0 + u * stride;
+            if (a >= nc) continue;
+            y[a] = v[u];
+            acc[0] = fma(v[u], v[u], acc[0]);
+        }
     }
     if (!norm2) return;
     const int ops[1] = {0};
@@ -309,7 +319,7 @@ int op_gather_apply(relcp_ctx *ctx, const relcp_constraints *cs, const double *U
                     int norm2) {
     const int64_t nc = cs->count;
     if (nc == 0) return RELCP_OK;
-    int grid = grid_for(nc, RELCP_NT, 8);
+    int grid = grid_for(nc, RELCP_NT, 4);
     k_gather<<<grid, RELCP_NT, 0, ctx->stream>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, U, scale, y,
                                                  norm2, ctx->partials.p, ctx->counter.p, ctx->st.p);
     CKL();

@@ -85,7 +85,7 @@ def load(build_if_missing: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
+    path = os.environ.get("RELCP_LIB", _build.LIB)  # tuning variants (tools/sweep)
     if not os.path.exists(path):
         if not build_if_missing:
             raise RuntimeError(f"librelcp.so missing at {path}; run paper_2506_14097_b200.build")

@@ -1,0 +1,43 @@
+"""Kernel micro-bench / ncu target: cfg5 A_0 at N bodies; a few Delassus
+applies then a capped LCP solve.  python tools/kbench.py [N] [iters]"""
+import os
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from gen import scenes  # noqa: E402
+from paper_2506_14097_b200 import relcp as R  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 2_000_000
+iters = int(sys.argv[2]) if len(sys.argv) > 2 else 200
+sc = scenes.cfg5(n=n)
+ctx = R.Context(dynamics=sc["dynamics"], dt=sc["dt"], box=list(sc["box"]), lcp_max_iter=iters, lcp_tol=1e-30,
+                power_iters=2)
+bodies = R.BodyState.from_scene(sc)
+cs = R.ConstraintStore(8 * n)
+ctx.generate_contacts(bodies, cs)
+ctx.prepare_operator(bodies, cs)
+nc = cs.count
+x = torch.rand(nc, dtype=torch.float64, device="cuda")
+y = torch.empty_like(x)
+for _ in range(3):
+    ctx.delassus_apply(bodies, cs, x, y)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(20):
+    ctx.delassus_apply(bodies, cs, x, y)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 20
+print(f"N={n} N_C={nc} apply {ms:.4f} ms  alg {(176 * nc + 152 * n) / ms / 1e6:.0f} GB/s", flush=True)
+ctx.set_timing(True)
+t = time.time()
+rep = ctx.solve_lcp(bodies, cs)
+st = ctx.stats()
+it = st["iter_timed"]
+print(f"solve {rep['iterations']} it in {time.time() - t:.3f}s; scatter {st['scatter_ms'] / it:.4f} ms "
+      f"gather {st['gather_ms'] / it:.4f} ms; iter alg "
+      f"{(216 * nc + 152 * n) / ((st['scatter_ms'] + st['gather_ms']) / it) / 1e6:.0f} GB/s", flush=True)
