@@ -214,8 +214,10 @@ static int snsd_flag_scan(relcp_ctx *ctx, const double *pos, double thresh, int 
     *nnonconv = 0;
     if (np == 0) return RELCP_OK;
     if (np >= (1ll << 31) - 1) return set_err(ctx, RELCP_E_ARG, "too many candidate pairs");
+    // pairs whose lower bound Phi >= F(d/|d|) is >= max(thresh, 0) can neither be
+    // flagged nor lower min(Phi) below 0: they are not solved (status 3)
     CKS(geo_snsd(ctx, np, ctx->pi.p, ctx->pj.p, pos, ctx->Sig.p, ctx->tphi.p, ctx->tn.p, ctx->tra.p, ctx->trb.p,
-                 ctx->tstat.p, np));
+                 ctx->tstat.p, np, thresh > 0.0 ? thresh : 0.0));
     k_flag<<<grid_for(np), RELCP_NT, 0, ctx->stream>>>(np, ctx->tphi.p, ctx->tstat.p, thresh, ctx->tflag.p,
                                                        ctx->partials.p, ctx->counter.p, ctx->red.p);
     CKL();
@@ -328,6 +330,8 @@ static int check_impl(relcp_ctx *ctx, const relcp_bodies *Ck, relcp_constraints 
     cs->count = base + nflag;
     // q_new = Phi(C_n) - s row . (W D lambda)   (b_n = A_n iota(x) - Phi~)
     CKS(op_row_dot_U(ctx, cs, base, base + nflag, ctx->U.p, -op_s(ctx), cs->q));
+    // keep the store sorted by (ia, ib, gen) (R18): stable merge of the new block
+    CKS(store_merge_appended(ctx, cs, base, nflag));
     ctx->op_nc = -1;
     CK(cudaStreamSynchronize(ctx->stream));
     return nnc > 0 ? RELCP_W_SNSD_NONCONV : RELCP_OK;
@@ -593,7 +597,7 @@ int relcp_snsd_pairs(relcp_ctx *ctx, const relcp_bodies *b, int64_t n_pairs, con
     if (!pi || !pj || !phi || !nrm || !ra || !rb || !status) return set_err(ctx, RELCP_E_ARG, "snsd: null output");
     CK(ctx->Sig.grow(6 * b->n));
     CKS(geo_shape_matrices(ctx, b->n, b->quat, b->axes, ctx->Sig.p));
-    CKS(geo_snsd(ctx, n_pairs, pi, pj, b->pos, ctx->Sig.p, phi, nrm, ra, rb, status, n_pairs));
+    CKS(geo_snsd(ctx, n_pairs, pi, pj, b->pos, ctx->Sig.p, phi, nrm, ra, rb, status, n_pairs, INFINITY));
     ctx->step_nb = -1;  // Sig overwritten
     return RELCP_OK;
 }

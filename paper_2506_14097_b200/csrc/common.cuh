@@ -67,6 +67,12 @@ struct relcp_ctx {
     // operator (prepared for `op_nc` rows and `op_nb` bodies)
     int64_t op_nc = -1, op_nb = -1;
     const void *op_key_ia = nullptr;
+    int op_sorted = 0;               // store sorted by ia: a-side read from the store (K6)
+    int64_t op_cap = 0;              // store plane stride
+    const double *op_n = nullptr, *op_ta = nullptr;
+    DevBuf<int> pa;                  // (nb + 1) a-side row pointer of a sorted store
+    DevBuf<int> mi;                  // merge scratch (3, rows)
+    DevBuf<double> md;               // merge scratch (13, rows)
     DevBuf<double> W;        // (nb, 8)
     DevBuf<int> row_ptr;     // (nb + 1)
     DevBuf<int> deg;         // (nb)  scratch
@@ -96,6 +102,7 @@ struct relcp_ctx {
     // pair temporaries
     DevBuf<double> tphi, tn, tra, trb;  // (P), (3,P) planes
     DevBuf<int> tflag, tstat;
+    DevBuf<int> multi;          // pairs needing the SNSD multistart (stage 2)
     DevBuf<long long> scan_ll;  // scan scratch
     DevBuf<long long> scan_tmp;
     DevBuf<int> cell_count, cell_start, cell_fill, cell_items, body_cell;
@@ -159,6 +166,9 @@ int op_gather_apply(relcp_ctx *ctx, const relcp_constraints *cs, const double *U
                     int norm2);
 int op_row_dot_U(relcp_ctx *ctx, const relcp_constraints *cs, int64_t begin, int64_t end, const double *U,
                  double coef, double *out_add);
+// store.cu
+int store_merge_appended(relcp_ctx *ctx, relcp_constraints *cs, int64_t n_old, int64_t m);
+int store_is_sorted_by_ia(relcp_ctx *ctx, const relcp_constraints *cs, int *sorted_host);
 // lcp.cu
 int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relcp_solve_report *rep);
 // scan.cu
@@ -167,5 +177,7 @@ int scan_exclusive_int(relcp_ctx *ctx, const int *in, int *out, int64_t n, int *
 // geometry.cu
 int geo_shape_matrices(relcp_ctx *ctx, int64_t nb, const double *quat, const double *axes, double *Sig);
 int geo_broadphase(relcp_ctx *ctx, int64_t nb, const double *pos, const double *rad, double margin);
+// reject_above: pairs whose rigorous lower bound Phi >= F(d/|d|) reaches it are
+// not solved (status 3, phi = the bound); +INFINITY = solve every pair.
 int geo_snsd(relcp_ctx *ctx, int64_t np, const int *pi, const int *pj, const double *pos, const double *Sig,
-             double *phi, double *nrm, double *ra, double *rb, int *status, int64_t planes);
+             double *phi, double *nrm, double *ra, double *rb, int *status, int64_t planes, double reject_above);

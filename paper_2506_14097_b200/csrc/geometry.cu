@@ -165,21 +165,62 @@ __device__ __forceinline__ bool better(double f, const double *n, double fb, con
     return n[2] < nb[2];
 }
 
-// Full SNSD of one pair.  Returns status 0 ok / 1 coincident / 2 not certified.
-__device__ int snsd_pair(const double *d, const Sym &Sa, const Sym &Sb, int n_dirs, double &phi, double *nout,
-                         double *ra, double *rb) {
+// SNSD status codes (k_snsd_* outputs)
+#define SNSD_OK 0
+#define SNSD_DEGENERATE 1  // coincident centres (R4)
+#define SNSD_NONCONV 2     // Newton not certified
+#define SNSD_BOUND 3       // quick reject: Phi >= F(d/|d|) >= reject threshold (phi = that lower bound)
+#define SNSD_MULTI 4       // internal: needs the multistart pass
+
+__device__ __forceinline__ void write_out(const Eval &E, const double *nb, double &phi, double *nout, double *ra,
+                                          double *rb) {
+    phi = E.f;
+    const double ia = 1.0 / E.ha, ib = 1.0 / E.hb;
+    for (int k = 0; k < 3; ++k) {
+        nout[k] = nb[k];
+        ra[k] = E.Sa_n[k] * ia;
+        rb[k] = -E.Sb_n[k] * ib;
+    }
+}
+
+// Stage 1 of one pair.  F is concave and 1-homogeneous on R^3, so
+// Phi >= F(d/|d|): if that bound is >= reject_above the pair cannot pass any
+// threshold below it (generation: cutoff; check: 0 > -eps) -> SNSD_BOUND.
+// Otherwise Newton from d/|d|; a maximum with F > 0 is global -> SNSD_OK /
+// SNSD_NONCONV; F <= 0 (overlap / touching) -> SNSD_MULTI (outputs hold the
+// Newton result as the incumbent for stage 2).
+__device__ int snsd_stage1(const double *d, const Sym &Sa, const Sym &Sb, double reject_above, double &phi,
+                           double *nout, double *ra, double *rb) {
     const double dn = sqrt(d3(d, d));
     if (!(dn >= 1e-12)) {
         phi = nan("");
         for (int k = 0; k < 3; ++k) nout[k] = ra[k] = rb[k] = nan("");
-        return 1;
+        return SNSD_DEGENERATE;
     }
-    const double dh[3] = {d[0] / dn, d[1] / dn, d[2] / dn};
-    double nb[3] = {dh[0], dh[1], dh[2]};
+    double nb[3] = {d[0] / dn, d[1] / dn, d[2] / dn};
     Eval Eb;
-    int st_best = newton_sphere(nb, d, dn, Sa, Sb, Eb) ? 0 : 2;
+    feval(nb, d, Sa, Sb, Eb);
+    if (Eb.f >= reject_above + 1e-12 * fmax(1.0, dn)) {
+        write_out(Eb, nb, phi, nout, ra, rb);
+        return SNSD_BOUND;
+    }
+    const int ok = newton_sphere(nb, d, dn, Sa, Sb, Eb);
+    feval(nb, d, Sa, Sb, Eb);
+    write_out(Eb, nb, phi, nout, ra, rb);
+    if (Eb.f > 0.0) return ok ? SNSD_OK : SNSD_NONCONV;
+    return ok ? SNSD_MULTI : -SNSD_MULTI;  // sign carries the incumbent's certification
+}
+
+// Stage 2 (overlap / touching): multistart from the best `n_dirs`-sample
+// directions against the incumbent (nb, status st_best) from stage 1.
+__device__ int snsd_stage2(const double *d, const Sym &Sa, const Sym &Sb, int n_dirs, double *nb, int st_best,
+                           double &phi, double *nout, double *ra, double *rb) {
+    const double dn = sqrt(d3(d, d));
+    const double dh[3] = {d[0] / dn, d[1] / dn, d[2] / dn};
+    Eval Eb;
+    feval(nb, d, Sa, Sb, Eb);
     double fb = Eb.f;
-    if (!(fb > 0.0)) {
+    {
         // overlap / touching: multistart from the best sampled directions
         constexpr int K = 4;
         double topf[K];
@@ -219,18 +260,12 @@ __device__ int snsd_pair(const double *d, const Sym &Sa, const Sym &Sb, int n_di
                 fb = Em.f;
                 nb[0] = m[0]; nb[1] = m[1]; nb[2] = m[2];
                 Eb = Em;
-                st_best = ok ? 0 : 2;
+                st_best = ok ? SNSD_OK : SNSD_NONCONV;
             }
         }
     }
     feval(nb, d, Sa, Sb, Eb);
-    phi = Eb.f;
-    const double ia = 1.0 / Eb.ha, ib = 1.0 / Eb.hb;
-    for (int k = 0; k < 3; ++k) {
-        nout[k] = nb[k];
-        ra[k] = Eb.Sa_n[k] * ia;
-        rb[k] = -Eb.Sb_n[k] * ib;
-    }
+    write_out(Eb, nb, phi, nout, ra, rb);
     return st_best;
 }
 
@@ -247,39 +282,89 @@ struct Box3 {
     double v[3];
 };
 
-// Batched SNSD over pairs; outputs as planes with stride `planes`.
-__global__ void __launch_bounds__(128) k_snsd(int64_t np, const int *__restrict__ pi, const int *__restrict__ pj,
-                                              const double *__restrict__ pos, const double *__restrict__ Sig,
-                                              Box3 box, int n_dirs, double *__restrict__ phi,
-                                              double *__restrict__ nrm, double *__restrict__ ra,
-                                              double *__restrict__ rb, int *__restrict__ status, int64_t planes) {
+__device__ __forceinline__ void pair_geom(int64_t k, const int *__restrict__ pi, const int *__restrict__ pj,
+                                          const double *__restrict__ pos, const double *__restrict__ Sig,
+                                          const Box3 &box, double *d, Sym &Sa, Sym &Sb) {
+    const int a = pi[k], b = pj[k];
+    min_image(pos + 3 * (int64_t)a, pos + 3 * (int64_t)b, box.v, d);
+    Sa = load_sym(Sig + 6 * (int64_t)a);
+    Sb = load_sym(Sig + 6 * (int64_t)b);
+}
+
+__device__ __forceinline__ void store_pair(int64_t k, int64_t planes, double f, const double *n, const double *r1,
+                                           const double *r2, double *__restrict__ phi, double *__restrict__ nrm,
+                                           double *__restrict__ ra, double *__restrict__ rb) {
+    phi[k] = f;
+    for (int c = 0; c < 3; ++c) {
+        nrm[c * planes + k] = n[c];
+        ra[c * planes + k] = r1[c];
+        rb[c * planes + k] = r2[c];
+    }
+}
+
+// K3/K10 stage 1 over all pairs; pairs needing the multistart are listed
+// (list order is scheduling dependent, the per-pair results are not).
+__global__ void __launch_bounds__(128) k_snsd_stage1(int64_t np, const int *__restrict__ pi,
+                                                     const int *__restrict__ pj, const double *__restrict__ pos,
+                                                     const double *__restrict__ Sig, Box3 box, double reject_above,
+                                                     double *__restrict__ phi, double *__restrict__ nrm,
+                                                     double *__restrict__ ra, double *__restrict__ rb,
+                                                     int *__restrict__ status, int64_t planes, int *multi,
+                                                     unsigned *n_multi) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < np; k += (int64_t)gridDim.x * blockDim.x) {
-        const int a = pi[k], b = pj[k];
         double d[3];
-        min_image(pos + 3 * (int64_t)a, pos + 3 * (int64_t)b, box.v, d);
-        const Sym Sa = load_sym(Sig + 6 * (int64_t)a), Sb = load_sym(Sig + 6 * (int64_t)b);
+        Sym Sa, Sb;
+        pair_geom(k, pi, pj, pos, Sig, box, d, Sa, Sb);
         double f, n[3], r1[3], r2[3];
-        int st = snsd_pair(d, Sa, Sb, n_dirs, f, n, r1, r2);
-        phi[k] = f;
-        for (int c = 0; c < 3; ++c) {
-            nrm[c * planes + k] = n[c];
-            ra[c * planes + k] = r1[c];
-            rb[c * planes + k] = r2[c];
+        int st = snsd_stage1(d, Sa, Sb, reject_above, f, n, r1, r2);
+        store_pair(k, planes, f, n, r1, r2, phi, nrm, ra, rb);
+        if (st == SNSD_MULTI || st == -SNSD_MULTI) {
+            multi[atomicAdd(n_multi, 1u)] = (int)k;
+            status[k] = st == SNSD_MULTI ? SNSD_OK : SNSD_NONCONV;  // incumbent's certification
+        } else {
+            status[k] = st;
         }
+    }
+}
+
+// Stage 2 over the listed (overlapping / touching) pairs: uniform work per thread.
+__global__ void __launch_bounds__(128) k_snsd_stage2(const int *__restrict__ multi, const unsigned *__restrict__ n_multi,
+                                                     const int *__restrict__ pi, const int *__restrict__ pj,
+                                                     const double *__restrict__ pos, const double *__restrict__ Sig,
+                                                     Box3 box, int n_dirs, double *__restrict__ phi,
+                                                     double *__restrict__ nrm, double *__restrict__ ra,
+                                                     double *__restrict__ rb, int *__restrict__ status,
+                                                     int64_t planes) {
+    const int64_t m = *n_multi;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = multi[i];
+        double d[3];
+        Sym Sa, Sb;
+        pair_geom(k, pi, pj, pos, Sig, box, d, Sa, Sb);
+        double nb[3] = {nrm[k], nrm[planes + k], nrm[2 * planes + k]};
+        double f, n[3], r1[3], r2[3];
+        const int st = snsd_stage2(d, Sa, Sb, n_dirs, nb, status[k], f, n, r1, r2);
+        store_pair(k, planes, f, n, r1, r2, phi, nrm, ra, rb);
         status[k] = st;
     }
 }
 
 int geo_snsd(relcp_ctx *ctx, int64_t np, const int *pi, const int *pj, const double *pos, const double *Sig,
-             double *phi, double *nrm, double *ra, double *rb, int *status, int64_t planes) {
+             double *phi, double *nrm, double *ra, double *rb, int *status, int64_t planes, double reject_above) {
     if (np <= 0) return RELCP_OK;
     Box3 bx;
     for (int k = 0; k < 3; ++k) bx.v[k] = ctx->p.box[k];
     int nd = ctx->p.n_dirs > 0 ? ctx->p.n_dirs : 256;
     if (nd > RELCP_MAX_DIRS) nd = RELCP_MAX_DIRS;
+    CK(ctx->multi.grow(np));
+    CK(cudaMemsetAsync(ctx->counter.p + 1, 0, sizeof(unsigned), ctx->stream));
     int64_t g = (np + 127) / 128;
     if (g > 148 * 64) g = 148 * 64;
-    k_snsd<<<(unsigned)g, 128, 0, ctx->stream>>>(np, pi, pj, pos, Sig, bx, nd, phi, nrm, ra, rb, status, planes);
+    k_snsd_stage1<<<(unsigned)g, 128, 0, ctx->stream>>>(np, pi, pj, pos, Sig, bx, reject_above, phi, nrm, ra, rb,
+                                                        status, planes, ctx->multi.p, ctx->counter.p + 1);
+    CKL();
+    k_snsd_stage2<<<148 * 8, 128, 0, ctx->stream>>>(ctx->multi.p, ctx->counter.p + 1, pi, pj, pos, Sig, bx, nd, phi,
+                                                    nrm, ra, rb, status, planes);
     CKL();
     return RELCP_OK;
 }

@@ -71,25 +71,28 @@ int op_build_W(relcp_ctx *ctx, const relcp_bodies *b, double *W) {
 }
 
 // ------------------------------------------------------------ CSR of D
-__global__ void k_degree(int64_t nc, const int32_t *__restrict__ ia, const int32_t *__restrict__ ib, int *deg,
-                         int64_t nb, int *bad) {
+// per-body counts of a-side rows (degA) and b-side rows (degB); may alias
+__global__ void k_degree(int64_t nc, const int32_t *__restrict__ ia, const int32_t *__restrict__ ib, int *degA,
+                         int *degB, int64_t nb, int *bad) {
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
         int i = ia[a], j = ib[a];
         if (i < 0 || j < 0 || i >= nb || j >= nb || i == j) { atomicExch(bad, 1); continue; }
-        atomicAdd(deg + i, 1);
-        atomicAdd(deg + j, 1);
+        atomicAdd(degA + i, 1);
+        atomicAdd(degB + j, 1);
     }
 }
 
 // entry key = side << 30 | constraint (side 0 = a, 1 = b); nc < 2^30
 #define EKEY_SIDE (1 << 30)
 __global__ void k_fill_slots(int64_t nc, const int32_t *__restrict__ ia, const int32_t *__restrict__ ib,
-                             const int *__restrict__ row_ptr, int *fill, int *ekey) {
+                             const int *__restrict__ row_ptr, int *fill, int *ekey, int b_only) {
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
         int i = ia[a], j = ib[a];
-        int si = row_ptr[i] + atomicAdd(fill + i, 1);
+        if (!b_only) {
+            int si = row_ptr[i] + atomicAdd(fill + i, 1);
+            ekey[si] = (int)a;  // side a
+        }
         int sj = row_ptr[j] + atomicAdd(fill + j, 1);
-        ekey[si] = (int)a;              // side a
         ekey[sj] = (int)a | EKEY_SIDE;  // side b
     }
 }
@@ -137,30 +140,41 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
     CK(ctx->U.grow(6 * nb));
     CK(ctx->ecid.grow(E > 0 ? E : 1));
     CK(ctx->ew.grow(6 * (E > 0 ? E : 1)));
+    CK(ctx->pa.grow(nb + 1));
     CKS(op_build_W(ctx, b, ctx->W.p));
+    int sorted = 0;
+    CKS(store_is_sorted_by_ia(ctx, cs, &sorted));
     CK(cudaMemsetAsync(ctx->deg.p, 0, sizeof(int) * (nb + 1), ctx->stream));
+    CK(cudaMemsetAsync(ctx->pa.p, 0, sizeof(int) * (nb + 1), ctx->stream));
     CK(cudaMemsetAsync(ctx->fill.p, 0, sizeof(int) * (nb + 1), ctx->stream));  // fill[nb] = bad flag
     if (nc > 0) {
-        k_degree<<<grid_for(nc), RELCP_NT, 0, ctx->stream>>>(nc, cs->ia, cs->ib, ctx->deg.p, nb, ctx->fill.p + nb);
+        k_degree<<<grid_for(nc), RELCP_NT, 0, ctx->stream>>>(nc, cs->ia, cs->ib, sorted ? ctx->pa.p : ctx->deg.p,
+                                                             ctx->deg.p, nb, ctx->fill.p + nb);
         CKL();
     }
     int total = 0;
     CKS(scan_exclusive_int(ctx, ctx->deg.p, ctx->row_ptr.p, nb + 1, &total));  // deg[nb] = 0
+    if (sorted) CKS(scan_exclusive_int(ctx, ctx->pa.p, ctx->pa.p, nb + 1, nullptr));  // in place
     int bad = 0;
     CK(cudaMemcpyAsync(&bad, ctx->fill.p + nb, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (bad) return set_err(ctx, RELCP_E_ARG, "prepare: body index out of range or ia == ib");
+    const int64_t Ee = sorted ? nc : E;  // CSR entries: b-side only when sorted
     if (nc > 0) {
         CK(cudaMemsetAsync(ctx->fill.p, 0, sizeof(int) * nb, ctx->stream));
         k_fill_slots<<<grid_for(nc), RELCP_NT, 0, ctx->stream>>>(nc, cs->ia, cs->ib, ctx->row_ptr.p, ctx->fill.p,
-                                                                 ctx->ecid.p);
+                                                                 ctx->ecid.p, sorted);
         CKL();
         k_sort_segments<<<grid_for(nb, 128), 128, 0, ctx->stream>>>(nb, ctx->row_ptr.p, ctx->ecid.p);
         CKL();
-        k_payload<<<grid_for(E), RELCP_NT, 0, ctx->stream>>>(E, cs->capacity, cs->n, cs->ta, cs->tb, ctx->ecid.p,
-                                                             ctx->ew.p);
+        k_payload<<<grid_for(Ee), RELCP_NT, 0, ctx->stream>>>(Ee, cs->capacity, cs->n, cs->ta, cs->tb, ctx->ecid.p,
+                                                              ctx->ew.p);
         CKL();
     }
+    ctx->op_sorted = sorted;
+    ctx->op_cap = cs->capacity;
+    ctx->op_n = cs->n;
+    ctx->op_ta = cs->ta;
     ctx->op_nc = nc;
     ctx->op_nb = nb;
     ctx->op_key_ia = cs->ia;
@@ -170,10 +184,17 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
 // ------------------------------------------------------------ scatter (K6)
 // U_b = W_b sum_{e in seg(b)} w_e * xeff(cid_e), xeff = proj ? max(0, x - alpha g) : x,
 // scaled by *xscale if given; optionally F_b = the raw sum.
-template <bool PROJ>
+//
+// SORTED (store sorted by ia, the library's own order, R18): body b's a-side
+// rows are the store rows [pa[b], pa[b+1]) and contribute -[n; t_a] x_eff read
+// straight from the store planes; row_ptr / ecid / ew then hold only the
+// b-side entries (+[n; t_b]).  Otherwise row_ptr / ecid / ew hold both sides.
+// Per-body order: a-side rows, then CSR entries -- fixed, deterministic.
+template <bool PROJ, bool SORTED>
 __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
     int64_t nb, int64_t E, const int *__restrict__ row_ptr, const int *__restrict__ ecid,
-    const double *__restrict__ ew, const double *__restrict__ x, const double *__restrict__ g,
+    const double *__restrict__ ew, const int *__restrict__ pa, int64_t cap, const double *__restrict__ cn,
+    const double *__restrict__ cta, const double *__restrict__ x, const double *__restrict__ g,
     const LcpState *__restrict__ st, const double *__restrict__ xscale, const double *__restrict__ W,
     double *__restrict__ U, double *__restrict__ Fout) {
     // contributions staged as 3 planes of double2 (components 01, 23, 45):
@@ -188,44 +209,59 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     double2(*c6)[SCATTER_TILE + 1] = sm[wl];
     const int64_t nwarp = (nb + 31) >> 5;
+    auto xeff = [&](int c) {
+        double xv = x[c];
+        if (PROJ) xv = fmax(0.0, xv - alpha * g[c]);
+        return xv * sc;
+    };
     for (int64_t w = blockIdx.x * (int64_t)SCATTER_WPB + wl; w < nwarp; w += (int64_t)gridDim.x * SCATTER_WPB) {
         const int64_t b0 = w << 5;
         const int64_t b = b0 + lane;
         const bool own = b < nb;
-        const int s = own ? row_ptr[b] : 0, t = own ? row_ptr[b + 1] : 0;
-        const int e0 = __shfl_sync(0xffffffffu, s, 0);
         const int last = nb - b0 < 32 ? (int)(nb - b0 - 1) : 31;
-        const int e1 = __shfl_sync(0xffffffffu, t, last);
         double f[6] = {0, 0, 0, 0, 0, 0};
-        for (int base = e0; base < e1; base += SCATTER_TILE) {
-            // stage the tile's contributions (coalesced loads)
+        // stream [e0, e1) of the warp in coalesced tiles; lane sums its [s, t)
+        auto tiles = [&](int s, int t, auto &&fetch) {
+            const int e0 = __shfl_sync(0xffffffffu, s, 0);
+            const int e1 = __shfl_sync(0xffffffffu, t, last);
+            for (int base = e0; base < e1; base += SCATTER_TILE) {
 #pragma unroll
-            for (int i = 0; i < SCATTER_TILE / 32; ++i) {
-                const int e = base + lane + 32 * i;
-                double v[6] = {0, 0, 0, 0, 0, 0};
-                if (e < e1) {
-                    const int c = ecid[e];
-                    double xv = x[c];
-                    if (PROJ) xv = fmax(0.0, xv - alpha * g[c]);
-                    xv *= sc;
+                for (int i = 0; i < SCATTER_TILE / 32; ++i) {
+                    const int e = base + lane + 32 * i;
+                    double v[6] = {0, 0, 0, 0, 0, 0};
+                    if (e < e1) fetch(e, v);
 #pragma unroll
-                    for (int k = 0; k < 6; ++k) v[k] = ew[k * E + e] * xv;
+                    for (int k = 0; k < 3; ++k) c6[k][lane + 32 * i] = make_double2(v[2 * k], v[2 * k + 1]);
                 }
+                __syncwarp();
+                const int lo = max(s, base) - base, hi = min(t, base + SCATTER_TILE) - base;
+                for (int j = lo; j < hi; ++j)
 #pragma unroll
-                for (int k = 0; k < 3; ++k) c6[k][lane + 32 * i] = make_double2(v[2 * k], v[2 * k + 1]);
+                    for (int k = 0; k < 3; ++k) {
+                        const double2 c = c6[k][j];
+                        f[2 * k] += c.x;
+                        f[2 * k + 1] += c.y;
+                    }
+                __syncwarp();
             }
-            __syncwarp();
-            // each lane sums its own body's entries inside the tile, in order
-            const int lo = max(s, base) - base, hi = min(t, base + SCATTER_TILE) - base;
-            for (int j = lo; j < hi; ++j)
+        };
+        if (SORTED) {
+            const int sa = own ? pa[b] : 0, ta_ = own ? pa[b + 1] : 0;
+            tiles(sa, ta_, [&](int e, double *v) {
+                const double xv = xeff(e);
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
-                    const double2 c = c6[k][j];
-                    f[2 * k] += c.x;
-                    f[2 * k + 1] += c.y;
+                    v[k] = -cn[k * cap + e] * xv;
+                    v[3 + k] = -cta[k * cap + e] * xv;
                 }
-            __syncwarp();
+            });
         }
+        const int s = own ? row_ptr[b] : 0, t = own ? row_ptr[b + 1] : 0;
+        tiles(s, t, [&](int e, double *v) {
+            const double xv = xeff(ecid[e]);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) v[k] = ew[k * E + e] * xv;
+        });
         // U_b = W_b F_b ; staged through shared memory for a coalesced AoS store
         double u[6] = {0, 0, 0, 0, 0, 0};
         if (own) {
@@ -260,19 +296,25 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
 
 int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int proj, const double *xscale_dev,
                double *U, double *F) {
-    const int64_t E = 2 * ctx->op_nc;
+    const int64_t E = ctx->op_sorted ? ctx->op_nc : 2 * ctx->op_nc;
     const int64_t nwarp = (nb + 31) / 32;
     int64_t grid = (nwarp + SCATTER_WPB - 1) / SCATTER_WPB;
     if (grid > (int64_t)RELCP_SM_COUNT * 64) grid = (int64_t)RELCP_SM_COUNT * 64;
     if (grid < 1) grid = 1;
-    if (proj)
-        k_scatter<true><<<(unsigned)grid, 32 * SCATTER_WPB, 0, ctx->stream>>>(nb, E, ctx->row_ptr.p, ctx->ecid.p,
-                                                                              ctx->ew.p, x, g, ctx->st.p, xscale_dev,
-                                                                              ctx->W.p, U, F);
-    else
-        k_scatter<false><<<(unsigned)grid, 32 * SCATTER_WPB, 0, ctx->stream>>>(nb, E, ctx->row_ptr.p, ctx->ecid.p,
-                                                                               ctx->ew.p, x, g, ctx->st.p, xscale_dev,
-                                                                               ctx->W.p, U, F);
+    const unsigned G = (unsigned)grid, T = 32 * SCATTER_WPB;
+    const int *pa = ctx->pa.p;
+    const int64_t cap = ctx->op_cap;
+    const double *cn = ctx->op_n, *cta = ctx->op_ta;
+#define SCATTER_ARGS nb, E, ctx->row_ptr.p, ctx->ecid.p, ctx->ew.p, pa, cap, cn, cta, x, g, ctx->st.p, xscale_dev, \
+                     ctx->W.p, U, F
+    if (ctx->op_sorted) {
+        if (proj) k_scatter<true, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+        else k_scatter<false, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+    } else {
+        if (proj) k_scatter<true, false><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+        else k_scatter<false, false><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+    }
+#undef SCATTER_ARGS
     CKL();
     return RELCP_OK;
 }

@@ -18,6 +18,20 @@ ctx = R.Context(dynamics=sc["dynamics"], dt=sc["dt"], box=list(sc["box"]), lcp_m
 bodies = R.BodyState.from_scene(sc)
 cs = R.ConstraintStore(8 * n)
 ctx.generate_contacts(bodies, cs)
+torch.cuda.synchronize()
+t = time.time()
+ctx.generate_contacts(bodies, cs)
+print(f"generate_contacts {1e3 * (time.time() - t):.1f} ms (pairs {ctx.get_pairs()[0].numel()}, rows {cs.count})",
+      flush=True)
+if len(sys.argv) > 3 and sys.argv[3] == "final":
+    # the step's final (largest, augmented) store; W at the step's C^k
+    init = {k: getattr(bodies, k).clone() for k in ("pos", "quat", "vel")}
+    ctx.set_params(max_recursions=2, lcp_max_iter=3000, lcp_tol=1e-8)
+    ctx.step(bodies, cs)
+    for k, v in init.items():
+        getattr(bodies, k).copy_(v)
+    ctx.set_params(lcp_max_iter=iters, lcp_tol=1e-30)
+    cs.lam.zero_()
 ctx.prepare_operator(bodies, cs)
 nc = cs.count
 x = torch.rand(nc, dtype=torch.float64, device="cuda")
