@@ -25,7 +25,7 @@
 #define SCATTER_WPB 8    // warps per block
 #define SCATTER_TILE 64  // entries staged per warp per tile
 #ifndef SCATTER_MINB
-#define SCATTER_MINB 6   // resident blocks per SM the register budget must allow (sweep: 6 best)
+#define SCATTER_MINB 4   // resident blocks per SM the register budget must allow (A/B: 4 best; 5, 6 spill)
 #endif
 
 // ------------------------------------------------------------ W blocks (SoA planes)
@@ -190,6 +190,10 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
 // straight from the store planes; row_ptr / ecid / ew then hold only the
 // b-side entries (+[n; t_b]).  Otherwise row_ptr / ecid / ew hold both sides.
 // Per-body order: a-side rows, then CSR entries -- fixed, deterministic.
+struct V6 {
+    double v[6];
+};
+
 template <bool PROJ, bool SORTED>
 __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
     int64_t nb, int64_t E, const int *__restrict__ row_ptr, const int *__restrict__ ecid,
@@ -228,10 +232,11 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
 #pragma unroll
                 for (int i = 0; i < SCATTER_TILE / 32; ++i) {
                     const int e = base + lane + 32 * i;
-                    double v[6] = {0, 0, 0, 0, 0, 0};
-                    if (e < e1) fetch(e, v);
+                    if (e < e1) {  // slots past e1 are never read
+                        const V6 v = fetch(e);
 #pragma unroll
-                    for (int k = 0; k < 3; ++k) c6[k][lane + 32 * i] = make_double2(v[2 * k], v[2 * k + 1]);
+                        for (int k = 0; k < 3; ++k) c6[k][lane + 32 * i] = make_double2(v.v[2 * k], v.v[2 * k + 1]);
+                    }
                 }
                 __syncwarp();
                 const int lo = max(s, base) - base, hi = min(t, base + SCATTER_TILE) - base;
@@ -247,20 +252,24 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
         };
         if (SORTED) {
             const int sa = own ? pa[b] : 0, ta_ = own ? pa[b + 1] : 0;
-            tiles(sa, ta_, [&](int e, double *v) {
+            tiles(sa, ta_, [&](int e) {
                 const double xv = xeff(e);
+                V6 v;
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
-                    v[k] = -cn[k * cap + e] * xv;
-                    v[3 + k] = -cta[k * cap + e] * xv;
+                    v.v[k] = -cn[k * cap + e] * xv;
+                    v.v[3 + k] = -cta[k * cap + e] * xv;
                 }
+                return v;
             });
         }
         const int s = own ? row_ptr[b] : 0, t = own ? row_ptr[b + 1] : 0;
-        tiles(s, t, [&](int e, double *v) {
+        tiles(s, t, [&](int e) {
             const double xv = xeff(ecid[e]);
+            V6 v;
 #pragma unroll
-            for (int k = 0; k < 6; ++k) v[k] = ew[k * E + e] * xv;
+            for (int k = 0; k < 6; ++k) v.v[k] = ew[k * E + e] * xv;
+            return v;
         });
         // U_b = W_b F_b ; staged through shared memory for a coalesced AoS store
         double u[6] = {0, 0, 0, 0, 0, 0};
