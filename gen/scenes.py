@@ -128,6 +128,167 @@ def cfg5(seed: int = 5, n: int = 2_000_000) -> dict:
                       dynamics=INERTIAL, name="cfg5" if n == 2_000_000 else f"cfg5-n{n}")
 
 
+def cfg3(seed: int = 3, n: int = 200_000, patch: int = 6, gap: float = 0.005, minor: float = 0.25,
+         growth: float = 0.01, dt: float = 1e-2) -> dict:
+    """Growing-colony-like monolayer (BASELINE cfg3, SURVEY §8(d) row-patch
+    construction): ellipsoids (a, 0.25, 0.25), a ~ U(0.5, 1.0), centres in
+    z = 0, symmetry axis in-plane.  P x P square patches, each with a director
+    theta_p ~ U(0, pi); inside a patch the bodies sit in rows along theta_p at
+    row spacing 2*minor + gap, tip to tip with gap `gap` (aligned bodies in
+    such rows are disjoint).  A body whose bounding circle (radius a) meets
+    the bounding circle of an already accepted body of another patch is
+    dropped (greedy, lattice order), so patches never overlap either.  The
+    construction runs in a disk sized for `n` bodies; the n bodies nearest
+    the centre are kept (ties by index).  Growth: a seeded half of the bodies
+    gets a += `growth` (the start-of-step axial growth), which creates the
+    small tip overlaps the step resolves.  Overdamped local drag (xi = 1),
+    dt = 1e-2, no external force, non-periodic.  Draw order: a per site, patch
+    directors, row offsets, growth set."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    # disk radius from the realised packing (~0.6 area fraction of a ~ 0.75 x 0.25 ellipses)
+    area_body = math.pi * 0.75 * minor
+    radius = math.sqrt(n * area_body / 0.55 / math.pi) + 4.0
+    side = 2.0 * radius
+    psz = side / patch
+    theta = rng.uniform(0.0, math.pi, size=(patch, patch))
+    pts, angs, majors, owner = [], [], [], []
+    for py in range(patch):
+        for px in range(patch):
+            th = theta[py, px]
+            u = np.array([math.cos(th), math.sin(th)])
+            v = np.array([-math.sin(th), math.cos(th)])
+            cx, cy = -radius + (px + 0.5) * psz, -radius + (py + 0.5) * psz
+            half = 0.75 * psz  # rows cover the rotated square patch
+            rows = np.arange(-half, half, 2 * minor + gap)
+            for rv in rows:
+                t = -half + rng.uniform(0.0, 1.0)
+                while t < half:
+                    a = rng.uniform(0.5, 1.0)
+                    c = np.array([cx, cy]) + (t + a) * u + rv * v
+                    t += 2 * a + gap
+                    if abs(c[0] - cx) > psz / 2 or abs(c[1] - cy) > psz / 2:
+                        continue
+                    if c[0] ** 2 + c[1] ** 2 > radius ** 2:
+                        continue
+                    pts.append(c)
+                    angs.append(th)
+                    majors.append(a)
+                    owner.append(py * patch + px)
+    pts = np.array(pts)
+    angs = np.array(angs)
+    majors = np.array(majors)
+    owner = np.array(owner)
+    # greedy cross-patch rejection with bounding circles (grid hashing)
+    keep = np.ones(len(pts), dtype=bool)
+    cell = 2.0
+    grid = {}
+    for i in range(len(pts)):
+        gx, gy = int(math.floor(pts[i, 0] / cell)), int(math.floor(pts[i, 1] / cell))
+        ok = True
+        for dx in (-1, 0, 1):
+            for dy in (-1, 0, 1):
+                for j in grid.get((gx + dx, gy + dy), ()):
+                    if owner[j] != owner[i]:
+                        d = pts[i] - pts[j]
+                        if d @ d < (majors[i] + majors[j]) ** 2:
+                            ok = False
+                            break
+                if not ok:
+                    break
+            if not ok:
+                break
+        if ok:
+            grid.setdefault((gx, gy), []).append(i)
+        else:
+            keep[i] = False
+    pts, angs, majors = pts[keep], angs[keep], majors[keep]
+    r2 = (pts ** 2).sum(1)
+    order = np.lexsort((np.arange(len(r2)), r2))[:n]
+    order = np.sort(order)  # keep construction (spatially coherent) order
+    if len(order) < n:
+        raise ValueError(f"cfg3 construction produced {len(order)} < {n} bodies")
+    pts, angs, majors = pts[order], angs[order], majors[order]
+    grow = np.zeros(n, dtype=bool)
+    grow[rng.permutation(n)[: n // 2]] = True
+    majors = majors + growth * grow
+    pos = np.zeros((n, 3))
+    pos[:, :2] = pts
+    quat = np.zeros((n, 4))
+    quat[:, 0] = np.cos(angs / 2)
+    quat[:, 3] = np.sin(angs / 2)
+    axes = np.stack([majors, np.full(n, minor), np.full(n, minor)], axis=1)
+    inv_mass, inv_inertia = _ellipsoid_mass_props(axes)
+    return dict(name="cfg3" if n == 200_000 else f"cfg3-n{n}", n=n, pos=pos, quat=quat, axes=axes,
+                vel=np.zeros((n, 6)), inv_mass=inv_mass, inv_inertia=inv_inertia,
+                kinematic=np.zeros(n, dtype=np.int32), box=np.zeros(3), dt=float(dt), dynamics=OVERDAMPED,
+                xi=1.0, cutoff=0.1, eps_ncp=1e-5, lcp_tol=1e-8, seed=seed, growing=grow,
+                area_fraction=float((axes[:, 0] * axes[:, 1]).sum() / (pts ** 2).sum(1).max()))
+
+
+def cfg4(seed: int = 4, n_side: int = 1000, R: float = 1.0, r: float = 0.2, pitch: float = 1.4,
+         c_max: int = 3, c_fixed: int | None = None, dt: float = 1e-3) -> dict:
+    """Taut chainmail-like constraint network (BASELINE cfg4):
+    n_side x n_side rings (torus R = 1, r = 0.2, rho = 1) on a square lattice
+    of pitch 1.4 R in the x-y plane, ring axes alternating x / y in a
+    checkerboard.  Every lattice link (a < b) gets c ~ U{1..c_max} (or
+    c_fixed) unilateral constraints with raw geometry drawn here:
+    normal n = normalize(-e_link + 0.25 g), g ~ N(0, I3) (n opposes
+    separation), lever arms r_a = R e_link + rho_a, r_b = -R e_link + rho_b,
+    rho uniform in a ball of radius 0.2, gap Phi_0 = 0 (taut).  Rows 0 and
+    n_side-1 (y index) are kinematic with velocity -1 / +1 along y; interior
+    bodies start with the affine field u_y = -1 + 2 i / (n_side - 1).
+    Inertial, dt = 1e-3.  Torus inertia: m = rho 2 pi^2 R r^2,
+    I_axis = m (R^2 + 3/4 r^2), I_diam = m (R^2 / 2 + 5/8 r^2), body z =
+    ring axis.  Rows are returned sorted by (ia, ib).  Draw order: counts,
+    then per row g, rho_a, rho_b."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    n = n_side * n_side
+    ii, jj = np.divmod(np.arange(n), n_side)  # body = i * n_side + j ; y index i, x index j
+    pos = np.stack([jj * pitch * R, ii * pitch * R, np.zeros(n)], axis=1)
+    quat = np.zeros((n, 4))
+    ax_x = (ii + jj) % 2 == 0
+    s = math.sqrt(0.5)
+    quat[ax_x] = [s, 0.0, s, 0.0]    # body z -> world x (rotation +90 deg about y)
+    quat[~ax_x] = [s, -s, 0.0, 0.0]  # body z -> world y (rotation -90 deg about x)
+    m = 2.0 * math.pi ** 2 * R * r * r
+    I_axis = m * (R * R + 0.75 * r * r)
+    I_diam = m * (0.5 * R * R + 0.625 * r * r)
+    inv_mass = np.full(n, 1.0 / m)
+    inv_inertia = np.tile([1.0 / I_diam, 1.0 / I_diam, 1.0 / I_axis], (n, 1))
+    kin = ((ii == 0) | (ii == n_side - 1)).astype(np.int32)
+    vel = np.zeros((n, 6))
+    vel[:, 1] = -1.0 + 2.0 * ii / (n_side - 1)
+    # links: horizontal (i, j)-(i, j+1), vertical (i, j)-(i+1, j)
+    b = np.arange(n).reshape(n_side, n_side)
+    la = np.concatenate([b[:, :-1].ravel(), b[:-1, :].ravel()])
+    lb = np.concatenate([b[:, 1:].ravel(), b[1:, :].ravel()])
+    e = np.concatenate([np.tile([1.0, 0.0, 0.0], (n_side * (n_side - 1), 1)),
+                        np.tile([0.0, 1.0, 0.0], (n_side * (n_side - 1), 1))])
+    cnt = (np.full(len(la), c_fixed) if c_fixed else rng.integers(1, c_max + 1, size=len(la)))
+    ia = np.repeat(la, cnt)
+    ib = np.repeat(lb, cnt)
+    el = np.repeat(e, cnt, axis=0)
+    m_rows = len(ia)
+    g = rng.standard_normal((m_rows, 3))
+    nrm = -el + 0.25 * g
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+
+    def ball(k):
+        v = rng.standard_normal((k, 3))
+        v /= np.linalg.norm(v, axis=1, keepdims=True)
+        return v * (0.2 * rng.uniform(0.0, 1.0, size=(k, 1)) ** (1.0 / 3.0))
+
+    ra = R * el + ball(m_rows)
+    rb = -R * el + ball(m_rows)
+    order = np.lexsort((ib, ia))  # stable: rows of one link keep draw order
+    net = dict(ia=ia[order].astype(np.int32), ib=ib[order].astype(np.int32), n=nrm[order], ra=ra[order],
+               rb=rb[order], phi=np.zeros(m_rows))
+    return dict(name="cfg4" if n_side == 1000 else f"cfg4-{n_side}", n=n, pos=pos, quat=quat,
+                axes=np.tile([R + r, R + r, r], (n, 1)), vel=vel, inv_mass=inv_mass, inv_inertia=inv_inertia,
+                kinematic=kin, box=np.zeros(3), dt=float(dt), dynamics=INERTIAL, xi=1.0, cutoff=0.1,
+                eps_ncp=1e-5, lcp_tol=1e-8, seed=seed, network=net)
+
+
 def random_constraint_network(n_bodies: int, n_con: int, seed: int,
                               dynamics: int = INERTIAL):
     """Random Jacobian data for operator-level tests: body pairs (a<b),

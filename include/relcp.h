@@ -178,6 +178,18 @@ int relcp_set_params(relcp_ctx *ctx, const relcp_params *p);
 int relcp_generate_contacts(relcp_ctx *ctx, const relcp_bodies *bodies, relcp_constraints *cs,
                             int64_t *n_out);
 
+/* Load a GIVEN constraint network (e.g. BASELINE cfg4's chainmail links)
+ * into the store, replacing its content: m rows with body ids ia < ib,
+ * normals n and lever arms ra = y_a - x_a, rb = y_b - x_b as (3, m) planes,
+ * gaps phi (m); all caller-owned device arrays.  Forms t_a = ra x n,
+ * t_b = rb x n, q = phi + dt row.U_free with U_free = vel
+ * (inertial, F_ext = 0) or 0 (overdamped), lambda = 0,
+ * gen = 0, in the given row order (rows sorted by (ia, ib) take the fast
+ * operator path).  Errors: E_ARG, E_CAPACITY (cs->count = m). */
+int relcp_load_constraints(relcp_ctx *ctx, const relcp_bodies *bodies, relcp_constraints *cs, int64_t m,
+                           const int32_t *ia, const int32_t *ib, const double *n, const double *ra,
+                           const double *rb, const double *phi);
+
 /* Build the operator for the current store: per-body W blocks at the bodies'
  * configuration (frozen C^k) and the body-major CSR of D.  Must be called
  * again after the caller edits ia/ib/n/ta/tb/count.  Generate, solve,

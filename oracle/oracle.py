@@ -238,6 +238,26 @@ def enumerate_lcp(A, q, tol=1e-12, all_solutions=False):
     return None
 
 
+def network_lcp(sc, tol: float = 1e-10, max_iter: int = 2_000_000):
+    """LCP of a given constraint network (BASELINE cfg4): rows t = r x n
+    (P:L1413), RHS q = Phi_0 + dt row . U_free with U_free = U^k (inertial,
+    F_ext = 0) or 0 (overdamped), A = s D^T W D.
+    Returns (x, g, info, W, rows dict)."""
+    net = sc["network"]
+    W = body_W(sc)
+    ta, tb = rows(net["n"], net["ra"], net["rb"])
+    ia, ib, nrm = net["ia"], net["ib"], net["n"]
+    dt = sc["dt"]
+    inertial = sc["dynamics"] == INERTIAL
+    U = sc["vel"] if inertial else np.zeros((sc["n"], 6))
+    rate = (-(nrm * U[ia, :3]).sum(1) - (ta * U[ia, 3:]).sum(1) + (nrm * U[ib, :3]).sum(1)
+            + (tb * U[ib, 3:]).sum(1))
+    q = net["phi"] + dt * rate
+    s = dt * dt if inertial else dt
+    x, g, info = bbpgd(W, ia, ib, nrm, ta, tb, s, q, None, tol, max_iter)
+    return x, g, info, W, dict(ia=ia, ib=ib, n=nrm, ta=ta, tb=tb, q=q, s=s)
+
+
 # ------------------------------------------------------------------- ReLCP
 
 def quat_rate_map(q, omega):

@@ -166,6 +166,28 @@ __global__ void k_append(int64_t np, const int *__restrict__ flag, const int *__
     }
 }
 
+// Given rows (relcp_load_constraints): t = r x n, q = phi, lambda = 0, gen = 0.
+__global__ void k_load_rows(int64_t m, const int32_t *__restrict__ ia_in, const int32_t *__restrict__ ib_in,
+                            const double *__restrict__ nrm, const double *__restrict__ ra,
+                            const double *__restrict__ rb, const double *__restrict__ phi, int64_t cap, int32_t *ia,
+                            int32_t *ib, int32_t *gv, double *n, double *ta, double *tb, double *phio, double *q,
+                            double *lam) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m; k += (int64_t)gridDim.x * blockDim.x) {
+        const double nx = nrm[k], ny = nrm[m + k], nz = nrm[2 * m + k];
+        const double ax = ra[k], ay = ra[m + k], az = ra[2 * m + k];
+        const double bx = rb[k], by = rb[m + k], bz = rb[2 * m + k];
+        ia[k] = ia_in[k];
+        ib[k] = ib_in[k];
+        gv[k] = 0;
+        n[k] = nx; n[cap + k] = ny; n[2 * cap + k] = nz;
+        ta[k] = ay * nz - az * ny; ta[cap + k] = az * nx - ax * nz; ta[2 * cap + k] = ax * ny - ay * nx;
+        tb[k] = by * nz - bz * ny; tb[cap + k] = bz * nx - bx * nz; tb[2 * cap + k] = bx * ny - by * nx;
+        phio[k] = phi[k];
+        q[k] = phi[k];
+        lam[k] = 0.0;
+    }
+}
+
 // ------------------------------------------------------------ helpers
 static int ensure_common(relcp_ctx *ctx, int64_t nb) {
     CK(ctx->Sig.grow(6 * nb));
@@ -425,6 +447,38 @@ int relcp_generate_contacts(relcp_ctx *ctx, const relcp_bodies *bodies, relcp_co
                                                         ctx->W.p, bodies->kinematic, ctx->ufree.p);
     CKL();
     return generate_impl(ctx, bodies, cs, n_out);
+}
+
+int relcp_load_constraints(relcp_ctx *ctx, const relcp_bodies *bodies, relcp_constraints *cs, int64_t m,
+                           const int32_t *ia, const int32_t *ib, const double *n, const double *ra,
+                           const double *rb, const double *phi) {
+    CKS(check_views(ctx, bodies, cs));
+    if (m < 0 || (m > 0 && (!ia || !ib || !n || !ra || !rb || !phi)))
+        return set_err(ctx, RELCP_E_ARG, "load_constraints: m >= 0 and all row arrays required");
+    if (m > cs->capacity) {
+        cs->count = m;
+        return set_err(ctx, RELCP_E_CAPACITY, "load_constraints: %lld rows, capacity %lld", (long long)m,
+                       (long long)cs->capacity);
+    }
+    if (ctx->p.dynamics == RELCP_INERTIAL && !bodies->vel)
+        return set_err(ctx, RELCP_E_ARG, "load_constraints: inertial dynamics needs vel");
+    const int64_t nb = bodies->n;
+    CKS(ensure_common(ctx, nb));
+    CKS(op_build_W(ctx, bodies, ctx->W.p));
+    k_ufree<<<grid_for(nb), RELCP_NT, 0, ctx->stream>>>(nb, ctx->p.dynamics, ctx->p.dt, bodies->vel, nullptr,
+                                                        ctx->W.p, bodies->kinematic, ctx->ufree.p);
+    CKL();
+    if (m > 0) {
+        k_load_rows<<<grid_for(m), RELCP_NT, 0, ctx->stream>>>(m, ia, ib, n, ra, rb, phi, cs->capacity, cs->ia, cs->ib,
+                                                               cs->gen, cs->n, cs->ta, cs->tb, cs->phi, cs->q,
+                                                               cs->lambda);
+        CKL();
+    }
+    cs->count = m;
+    CKS(op_row_dot_U(ctx, cs, 0, m, ctx->ufree.p, ctx->p.dt, cs->q));  // q = Phi_0 + dt row.U_free
+    ctx->op_nc = -1;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return RELCP_OK;
 }
 
 int relcp_prepare_operator(relcp_ctx *ctx, const relcp_bodies *bodies, const relcp_constraints *cs) {

@@ -26,7 +26,7 @@ W_MAX_ITER, W_RECURSION_CAP, W_SNSD_NONCONV = 1, 2, 3
 EXPORTS = ["relcp_default_params", "relcp_create", "relcp_destroy", "relcp_last_error", "relcp_set_params",
            "relcp_generate_contacts", "relcp_prepare_operator", "relcp_delassus_apply", "relcp_wrench",
            "relcp_solve_lcp", "relcp_check_and_augment", "relcp_step", "relcp_get_pairs", "relcp_snsd_pairs",
-           "relcp_get_stats", "relcp_reset_stats", "relcp_set_timing"]
+           "relcp_get_stats", "relcp_reset_stats", "relcp_set_timing", "relcp_load_constraints"]
 
 P = ctypes.c_void_p
 i32, i64, f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
@@ -113,6 +113,8 @@ def load(build_if_missing: bool = True):
     L.relcp_get_stats.argtypes = [P, ctypes.POINTER(Stats)]
     L.relcp_reset_stats.argtypes = [P]
     L.relcp_set_timing.argtypes = [P, i32]
+    L.relcp_load_constraints.argtypes = [P, ctypes.POINTER(Bodies), ctypes.POINTER(Constraints), i64, P, P, P, P,
+                                         P, P]
     for name in EXPORTS:
         if name not in ("relcp_default_params", "relcp_last_error"):
             getattr(L, name).restype = ctypes.c_int
@@ -262,6 +264,23 @@ class Context:
         cs.sync_from(cv)
         self._check(rc)
         return int(n.value), rc
+
+    def load_constraints(self, bodies: BodyState, cs: ConstraintStore, ia, ib, n, ra, rb, phi):
+        """Given network rows; n, ra, rb as (m, 3) (host or device), ia, ib, phi (m,)."""
+        dev = "cuda"
+        t32 = lambda a: torch.as_tensor(np.asarray(a) if not torch.is_tensor(a) else a, dtype=torch.int32,
+                                        device=dev).contiguous()
+        tpl = lambda a: torch.as_tensor(np.asarray(a) if not torch.is_tensor(a) else a, dtype=torch.float64,
+                                        device=dev).T.contiguous()
+        ia_t, ib_t = t32(ia), t32(ib)
+        n_t, ra_t, rb_t = tpl(n), tpl(ra), tpl(rb)
+        phi_t = torch.as_tensor(np.asarray(phi) if not torch.is_tensor(phi) else phi, dtype=torch.float64,
+                                device=dev).contiguous()
+        bv, cv = bodies.view(), cs.view()
+        rc = self.L.relcp_load_constraints(self.h, ctypes.byref(bv), ctypes.byref(cv), ia_t.numel(), _ptr(ia_t),
+                                           _ptr(ib_t), _ptr(n_t), _ptr(ra_t), _ptr(rb_t), _ptr(phi_t))
+        cs.sync_from(cv)
+        self._check(rc)
 
     def prepare_operator(self, bodies: BodyState, cs: ConstraintStore):
         bv, cv = bodies.view(), cs.view()

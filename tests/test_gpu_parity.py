@@ -335,3 +335,50 @@ def test_step_deterministic(R):
         ctx.step(bodies, cs)
         out.append((bodies.pos.clone(), bodies.vel.clone(), cs.lam[:cs.count].clone()))
     assert all(torch.equal(a, b) for a, b in zip(out[0], out[1]))
+
+
+# ------------------------------------------------------------ cfg3 / cfg4 recipes
+
+@pytest.mark.parametrize("c_fixed", [None, 3])
+def test_cfg4_network_lcp_parity(orc, R, c_fixed):
+    """Given chainmail network (cfg4 recipe, 16 x 16 rings): rows, q, and the
+    solved LCP against the oracle.  c = 3 per link makes N_C exceed the free
+    DOFs, so lambda is not unique: compare D lambda and g (Lemma 5, R13)."""
+    sc = scenes.cfg4(n_side=16, c_fixed=c_fixed)
+    x_ref, g_ref, info, W, rw = orc.network_lcp(sc, 1e-10)
+    ctx = _ctx(R, sc, lcp_tol=1e-10, lcp_max_iter=2_000_000)
+    bodies = R.BodyState.from_scene(sc)
+    net = sc["network"]
+    cs = R.ConstraintStore(len(net["ia"]) + 7)
+    ctx.load_constraints(bodies, cs, net["ia"], net["ib"], net["n"], net["ra"], net["rb"], net["phi"])
+    c = cs.to_numpy()
+    assert np.max(np.abs(c["ta"] - rw["ta"])) <= 1e-15 and np.max(np.abs(c["tb"] - rw["tb"])) <= 1e-15
+    assert np.max(np.abs(c["q"] - rw["q"])) <= 1e-15
+    rep = ctx.solve_lcp(bodies, cs)
+    assert rep["converged"] and rep["residual"] <= 1e-10
+    lam = cs.lam[:cs.count].cpu().numpy()
+    g = cs.g[:cs.count].cpu().numpy()
+    assert np.all(lam >= 0)
+    gs = max(1e-300, np.max(np.abs(g_ref)))
+    assert np.max(np.abs(g - g_ref)) <= 1e-6 * gs + 1e-9
+    # unique by Lemma 5: U = W D lambda everywhere, D lambda on bodies with W > 0
+    F_ref, U_ref = orc.wrench(W, rw["ia"], rw["ib"], rw["n"], rw["ta"], rw["tb"], x_ref)
+    F = torch.empty(sc["n"], 6, dtype=torch.float64, device="cuda")
+    U = torch.empty_like(F)
+    ctx.prepare_operator(bodies, cs)
+    ctx.wrench(bodies, cs, cs.lam[:cs.count].contiguous(), F, U)
+    free = sc["kinematic"] == 0
+    assert np.max(np.abs(U.cpu().numpy() - U_ref)) <= 1e-6 * np.max(np.abs(U_ref))
+    assert np.max(np.abs(F.cpu().numpy()[free] - F_ref[free])) <= 1e-6 * np.max(np.abs(F_ref[free]))
+    if c_fixed is None:
+        assert np.max(np.abs(lam - x_ref)) <= 1e-6 * np.max(np.abs(x_ref))
+    assert np.all(U.cpu().numpy()[~free] == 0)  # kinematic rows: W = 0
+
+
+def test_cfg3_step_parity(orc, R):
+    """Planar growing colony (cfg3 recipe, 800 bodies, overdamped)."""
+    sc = scenes.cfg3(n=800)
+    r, rep, g = _compare_step(orc, R, sc, max_recursions=3)
+    # planar symmetry: normals and torque arms stay in / normal to z = 0
+    assert np.max(np.abs(g["n"][:, 2])) < 1e-11
+    assert np.max(np.abs(r["pos"][:, 2])) < 1e-11
