@@ -179,11 +179,16 @@ def run_ours(args, rank, world, dist):
     clocks = Clocks(dev.index) if rank == 0 else None
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    prof = os.environ.get("RELCP_PROFILE_TIMED") == "1"  # ncu --profile-from-start off: timed region only
+    if prof:
+        torch.cuda.profiler.start()
     e0.record()
     for _ in range(args.steps):
         one_step()
     e1.record()
     torch.cuda.synchronize()
+    if prof:
+        torch.cuda.profiler.stop()
     ms = e0.elapsed_time(e1)
     clk = clocks.stop() if clocks else None
     ctx.set_timing(False)
