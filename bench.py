@@ -217,6 +217,12 @@ def run_ours(args, rank, world, dist):
     peak_src = "measured" if peak else "fallback"
     peak = peak or 6650.0
     achieved = nbytes / (it_ms / 1e3) / 1e9 if it_ms > 0 else None
+    # DRAM traffic per iteration from the committed ncu --set full capture (K6 + K7)
+    traffic = traffic_ratio = traffic_nc = None
+    tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tr_path):
+        tr = json.load(open(tr_path))
+        traffic, traffic_ratio, traffic_nc = tr["dram_bytes_per_iteration"], tr["ratio"], tr["n_c"]
 
     # Delassus apply GB/s at A_0 and at the final (largest) store
     apply = {}
@@ -294,7 +300,8 @@ def run_ours(args, rank, world, dist):
                     lcp_tol=1e-8, parallelism=f"replicas{world}", l2="inputs larger than L2 (GB working set)",
                     n_c=last.get("n_c"), lcp_iters=last.get("iterations"), n_pairs=last.get("n_pairs")),
         roofline=dict(bound="hbm", kernel="LCP iteration (K6 scatter + K7 gather)", achieved=achieved, peak=peak,
-                      unit="GB/s", frac=(achieved / peak) if achieved else None, traffic=None,
+                      unit="GB/s", frac=(achieved / peak) if achieved else None, traffic=traffic,
+                      traffic_n_c=traffic_nc, traffic_over_algorithmic=traffic_ratio,
                       peak_source=peak_src, frac_of_8TBps=(achieved / 8000.0) if achieved else None,
                       iter_ms=it_ms / max(1, stats["iter_timed"]), scatter_ms_total=stats["scatter_ms"],
                       gather_ms_total=stats["gather_ms"], share_of_step=it_ms / ms),
