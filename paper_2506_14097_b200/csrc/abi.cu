@@ -390,6 +390,15 @@ int relcp_create(relcp_ctx **out, const relcp_params *p, void *cuda_stream) {
     relcp_ctx *ctx = new relcp_ctx();
     ctx->p = *p;
     ctx->stream = (cudaStream_t)cuda_stream;
+    if (!ctx->stream) {
+        // the legacy default stream cannot be captured into CUDA graphs: use an
+        // own BLOCKING stream (implicitly ordered with the legacy stream)
+        if (cudaStreamCreate(&ctx->stream) != cudaSuccess) {
+            delete ctx;
+            return RELCP_E_CUDA;
+        }
+        ctx->own_stream = 1;
+    }
     ctx->err[0] = 0;
     auto fail = [&](int code) {
         relcp_destroy(ctx);
@@ -421,6 +430,7 @@ int relcp_destroy(relcp_ctx *ctx) {
     if (ctx->ev_ready)
         for (int k = 0; k < 3 * 64; ++k) cudaEventDestroy(ctx->ev[k]);
     if (ctx->st_host) cudaFreeHost(ctx->st_host);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->red_host) cudaFreeHost(ctx->red_host);
     delete ctx;
     return RELCP_OK;

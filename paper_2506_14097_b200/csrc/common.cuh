@@ -62,6 +62,7 @@ struct LcpState {
 struct relcp_ctx {
     relcp_params p;
     cudaStream_t stream;
+    int own_stream = 0;  // created by relcp_create (caller passed the legacy stream)
     char err[512];
 
     // operator (prepared for `op_nc` rows and `op_nb` bodies)

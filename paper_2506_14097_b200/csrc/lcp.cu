@@ -208,7 +208,23 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
         }
     }
     long long it_before = 0;
-    int pending = 0;
+    int pending = 0, batches = 0;
+    cudaGraphExec_t gexec = nullptr;
+    // `batch` BB iterations: K6 (scatter + projection) then K7 (gather + update)
+    auto enqueue_batch = [&]() -> int {
+        for (int j = 0; j < batch; ++j) {
+            // per-iteration events only in timing mode, which never captures graphs
+            if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j], st));
+            CKS(op_scatter(ctx, nb, cs->lambda, cs->g, 1, nullptr, ctx->U.p, nullptr));
+            if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j + 1], st));
+            k_lcp_iter<<<gridc, RELCP_NT, 0, st>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->U.p,
+                                                   s, cs->q, cs->lambda, cs->g, ctx->partials.p, ctx->counter.p,
+                                                   ctx->st.p);
+            CKL();
+            if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j + 2], st));
+        }
+        return RELCP_OK;
+    };
     for (;;) {
         CK(cudaMemcpyAsync(ctx->st_host, ctx->st.p, sizeof(LcpState), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -226,18 +242,29 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
         }
         it_before = ctx->st_host->iter;
         if (ctx->st_host->done) break;
-        for (int j = 0; j < batch; ++j) {
-            if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j], st));
-            CKS(op_scatter(ctx, nb, cs->lambda, cs->g, 1, nullptr, ctx->U.p, nullptr));
-            if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j + 1], st));
-            k_lcp_iter<<<gridc, RELCP_NT, 0, st>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->U.p,
-                                                   s, cs->q, cs->lambda, cs->g, ctx->partials.p, ctx->counter.p,
-                                                   ctx->st.p);
-            CKL();
-            if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j + 2], st));
+        if (!gexec && batches >= 1 && !ctx->timing) {
+            // the solve runs long: capture one batch as a CUDA graph, replay it
+            cudaGraph_t graph = nullptr;
+            CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            const int rc = enqueue_batch();
+            cudaError_t ec = cudaStreamEndCapture(st, &graph);
+            ctx->launches -= 2 * batch;  // captured, not executed
+            if (rc < 0) return rc;
+            CK(ec);
+            ec = cudaGraphInstantiate(&gexec, graph, 0);
+            cudaGraphDestroy(graph);
+            CK(ec);
         }
+        if (gexec) {
+            CK(cudaGraphLaunch(gexec, st));
+            ctx->launches += 2 * batch;
+        } else {
+            CKS(enqueue_batch());
+        }
+        ++batches;
         pending = batch;
     }
+    if (gexec) CK(cudaGraphExecDestroy(gexec));
     k_objective<<<gridc, RELCP_NT, 0, st>>>(nc, cs->lambda, cs->g, cs->q, ctx->partials.p, ctx->counter.p, ctx->st.p);
     CKL();
     CK(cudaMemcpyAsync(ctx->st_host, ctx->st.p, sizeof(LcpState), cudaMemcpyDeviceToHost, st));

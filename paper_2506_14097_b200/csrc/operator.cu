@@ -23,7 +23,9 @@
 #include "reduce.cuh"
 
 #define SCATTER_WPB 8    // warps per block
+#ifndef SCATTER_TILE
 #define SCATTER_TILE 64  // entries staged per warp per tile
+#endif
 #ifndef SCATTER_MINB
 #define SCATTER_MINB 4   // resident blocks per SM the register budget must allow (A/B: 4 best; 5, 6 spill)
 #endif

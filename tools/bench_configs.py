@@ -93,6 +93,15 @@ def run(name):
     rep = ctx.step(bodies, cs)  # warm-up
     for k, v in init.items():
         getattr(bodies, k).copy_(v)
+    # step time without per-iteration events (LCP batches replayed as CUDA graphs)
+    a, b = ev(), ev()
+    a.record()
+    ctx.step(bodies, cs)
+    b.record()
+    torch.cuda.synchronize()
+    out["step_ms_graphs"] = a.elapsed_time(b)
+    for k, v in init.items():
+        getattr(bodies, k).copy_(v)
     ctx.reset_stats()
     ctx.set_timing(True)
     a, b = ev(), ev()
