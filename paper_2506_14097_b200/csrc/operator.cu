@@ -22,12 +22,14 @@
 #include "common.cuh"
 #include "reduce.cuh"
 
-#define SCATTER_WPB 8    // warps per block
+#ifndef SCATTER_WPB
+#define SCATTER_WPB 4    // warps per block (same-box A/B: 4 x 8 blocks beats 8 x 4)
+#endif
 #ifndef SCATTER_TILE
 #define SCATTER_TILE 64  // entries staged per warp per tile
 #endif
 #ifndef SCATTER_MINB
-#define SCATTER_MINB 4   // resident blocks per SM the register budget must allow (A/B: 4 best; 5, 6 spill)
+#define SCATTER_MINB 8   // resident blocks per SM the register budget must allow (64 regs at 4 warps)
 #endif
 
 // ------------------------------------------------------------ W blocks (SoA planes)
@@ -195,6 +197,8 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
 struct V6 {
     double v[6];
 };
+// the U / F transpose reuses a warp's staging area: 2 x 32 x 6 doubles
+static_assert(3 * (SCATTER_TILE + 1) * 2 >= 2 * 192, "SCATTER_TILE too small for the U/F staging");
 
 template <bool PROJ, bool SORTED>
 __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
