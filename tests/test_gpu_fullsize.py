@@ -1,0 +1,165 @@
+"""GPU checks at BASELINE.json's FULL sizes, in the launch configuration
+bench.py times (same kernels, same grids).  The oracle cannot run whole
+2M-body steps, so these compare (a) outputs the oracle computes completely
+from generator inputs (Delassus apply / wrench on a 2M-body, 10M-row
+network), (b) sampled outputs the oracle computes one by one (SNSD of sampled
+candidate pairs, broadphase inside a sub-box), and (c) properties that hold
+at any size: sorted store, q retention, lambda >= 0, KKT residual,
+Newton's third law (linear momentum is conserved), planar
+symmetry of cfg3, zero velocity change of kinematic bodies in cfg4."""
+import numpy as np
+import pytest
+
+from gen import scenes
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def R():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test collected without a CUDA device")
+    from paper_2506_14097_b200 import relcp
+    relcp.load()
+    return relcp
+
+
+def _ctx(R, sc, **kw):
+    p = dict(dynamics=sc["dynamics"], dt=sc["dt"], cutoff=sc["cutoff"], eps_ncp=sc["eps_ncp"],
+             box=list(sc["box"]), xi=sc.get("xi", 1.0))
+    p.update(kw)
+    return R.Context(**p)
+
+
+@pytest.mark.parametrize("shuffled", [False, True])
+def test_fullsize_delassus_apply(orc, R, shuffled):
+    """2M bodies, 10M rows (cfg5 scale): every output against the oracle at
+    1e-12; the shuffled store exercises the general (unsorted) CSR path."""
+    b, ia, ib, n, ra, rb = scenes.random_constraint_network(2_000_000, 10_000_000, 77)
+    if shuffled:
+        p = np.random.default_rng(5).permutation(len(ia))
+        ia, ib, n, ra, rb = ia[p], ib[p], n[p], ra[p], rb[p]
+    ta, tb = np.cross(ra, n), np.cross(rb, n)
+    W = orc.body_W(b)
+    x = np.random.default_rng(1).standard_normal(len(ia))
+    s = 1e-6
+    y_ref = orc.delassus_apply(W, ia, ib, n, ta, tb, s, x)
+    F_ref, U_ref = orc.wrench(W, ia, ib, n, ta, tb, x)
+    ctx = _ctx(R, dict(dynamics=0, dt=1e-3, cutoff=0.1, eps_ncp=1e-5, box=[0, 0, 0]))
+    bodies = R.BodyState.from_scene(b)
+    cs = R.ConstraintStore.from_rows(ia, ib, n, ta, tb)
+    ctx.prepare_operator(bodies, cs)
+    xd = torch.as_tensor(x, device="cuda")
+    yd = torch.empty_like(xd)
+    ctx.delassus_apply(bodies, cs, xd, yd, s)
+    assert np.max(np.abs(yd.cpu().numpy() - y_ref)) <= 1e-12 * np.max(np.abs(y_ref))
+    F = torch.empty(b["n"], 6, dtype=torch.float64, device="cuda")
+    U = torch.empty_like(F)
+    ctx.wrench(bodies, cs, xd, F, U)
+    assert np.max(np.abs(F.cpu().numpy() - F_ref)) <= 1e-12 * np.max(np.abs(F_ref))
+    assert np.max(np.abs(U.cpu().numpy() - U_ref)) <= 1e-12 * np.max(np.abs(U_ref))
+
+
+@pytest.fixture(scope="module")
+def cfg5_full():
+    return scenes.cfg5()
+
+
+def test_fullsize_cfg5_generate(orc, R, cfg5_full):
+    sc = cfg5_full
+    ctx = _ctx(R, sc)
+    bodies = R.BodyState.from_scene(sc)
+    cs = R.ConstraintStore(12 * sc["n"])
+    n0, _ = ctx.generate_contacts(bodies, cs)
+    pi, pj = (t.cpu().numpy() for t in ctx.get_pairs())
+    assert 20e6 < len(pi) < 23e6 and 5.0e6 < n0 < 5.6e6
+    key = pi.astype(np.int64) << 32 | pj
+    assert np.all(pi < pj) and np.all(np.diff(key) > 0)
+    # broadphase inside a 20^3 sub-box: exact against the oracle's O(N^2) scan
+    inside = np.all(sc["pos"] < 20.0, axis=1)
+    S = np.flatnonzero(inside)
+    ri, rj = orc.broadphase(sc["pos"][S], sc["axes"][S].max(1), sc["box"], sc["cutoff"], "brute")
+    ref = set(zip(S[ri].tolist(), S[rj].tolist()))
+    mask = inside[pi] & inside[pj]
+    got = set(zip(pi[mask].tolist(), pj[mask].tolist()))
+    assert len(ref) > 1000 and got == ref
+    # sampled SNSD: 3000 candidate pairs, oracle one by one from the generator's bodies
+    rng = np.random.default_rng(0)
+    k = rng.choice(len(pi), 3000, replace=False)
+    phi_r, n_r, *_ = orc.snsd(sc["pos"], sc["quat"], sc["axes"], sc["box"], pi[k], pj[k])
+    phi, nn, ra, rb, st = ctx.snsd_pairs(bodies, pi[k], pj[k])
+    phi = phi.cpu().numpy()
+    assert np.max(np.abs(phi - phi_r)) <= 1e-12 * 4
+    ok = np.abs(phi_r) > 1e-9
+    assert np.max(np.abs(nn.cpu().numpy().T[ok] - n_r[ok])) <= 1e-10
+    # the store holds exactly the candidates with Phi < cutoff: check the sample
+    c = cs.to_numpy()
+    rows = set(zip(c["ia"].tolist(), c["ib"].tolist()))
+    for a, b2, f in zip(pi[k], pj[k], phi_r):
+        if abs(f - sc["cutoff"]) > 1e-10:
+            assert ((int(a), int(b2)) in rows) == (f < sc["cutoff"])
+
+
+def test_fullsize_cfg5_step_invariants(R, cfg5_full):
+    """The bench workload (2 recursions, 3000-iteration LCP cap)."""
+    sc = cfg5_full
+    ctx = _ctx(R, sc, lcp_tol=1e-8, lcp_max_iter=3000, max_recursions=2)
+    bodies = R.BodyState.from_scene(sc)
+    cs = R.ConstraintStore(12 * sc["n"])
+    ctx.generate_contacts(bodies, cs)
+    q0 = cs.q[:cs.count].clone()
+    key0 = (cs.ia[:cs.count].long() << 32) | cs.ib[:cs.count].long()
+    rep = ctx.step(bodies, cs)
+    assert rep["n_c"][0] == len(q0) and rep["recursions"] == 2
+    m = cs.count
+    ia, ib, gen = cs.ia[:m].long(), cs.ib[:m].long(), cs.gen[:m].long()
+    key = (ia << 32) | ib
+    # sorted by (ia, ib, gen) (R18)
+    assert bool(torch.all(key[1:] >= key[:-1]))
+    same = key[1:] == key[:-1]
+    assert bool(torch.all(gen[1:][same] > gen[:-1][same]))
+    # q retention: generation-0 rows keep q_0
+    g0 = gen == 0
+    assert torch.equal(key[g0], key0) and torch.equal(cs.q[:m][g0], q0)
+    lam = cs.lam[:m]
+    assert bool(torch.all(lam >= 0))
+    # Newton's third law: total linear momentum unchanged (no external force)
+    mass = torch.as_tensor(1.0 / sc["inv_mass"], device="cuda")
+    v0 = torch.as_tensor(sc["vel"][:, :3], device="cuda")
+    dP = ((bodies.vel[:, :3] - v0) * mass[:, None]).sum(0)
+    scale = ((bodies.vel[:, :3] - v0).abs() * mass[:, None]).sum()
+    assert float(dP.abs().max()) <= 1e-12 * float(scale)
+
+
+def test_fullsize_cfg4_lcp(R):
+    sc = scenes.cfg4()
+    net = sc["network"]
+    ctx = _ctx(R, sc, lcp_tol=1e-8, lcp_max_iter=20000)
+    bodies = R.BodyState.from_scene(sc)
+    cs = R.ConstraintStore(len(net["ia"]) + 16)
+    ctx.load_constraints(bodies, cs, net["ia"], net["ib"], net["n"], net["ra"], net["rb"], net["phi"])
+    rep = ctx.solve_lcp(bodies, cs)
+    assert rep["converged"] and rep["residual"] <= 1e-8
+    m = cs.count
+    lam, g = cs.lam[:m], cs.g[:m]
+    assert bool(torch.all(lam >= 0)) and float(torch.minimum(lam, g).abs().max()) <= 1e-8
+    U = torch.empty(sc["n"], 6, dtype=torch.float64, device="cuda")
+    ctx.prepare_operator(bodies, cs)
+    ctx.wrench(bodies, cs, lam.contiguous(), None, U)
+    kin = torch.as_tensor(sc["kinematic"], device="cuda") != 0
+    assert int(kin.sum()) == 2000 and float(U[kin].abs().max()) == 0.0
+    assert 0.4 < float((lam > 0).double().mean()) < 0.9
+
+
+def test_fullsize_cfg3_step_planar(R):
+    sc = scenes.cfg3()
+    ctx = _ctx(R, sc, lcp_tol=1e-8, lcp_max_iter=3000, max_recursions=3)
+    bodies = R.BodyState.from_scene(sc)
+    cs = R.ConstraintStore(12 * sc["n"])
+    rep = ctx.step(bodies, cs)
+    assert 2.5 < 2 * rep["n_c"][0] / sc["n"] < 4.5  # ~3 contacts per body (BASELINE cfg3)
+    m = cs.count
+    assert float(cs.n[2, :m].abs().max()) < 1e-11
+    assert float(bodies.pos[:, 2].abs().max()) < 1e-11
+    assert bool(torch.all(cs.lam[:m] >= 0))
