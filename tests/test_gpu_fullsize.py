@@ -159,7 +159,15 @@ def test_fullsize_cfg3_step_planar(R):
     cs = R.ConstraintStore(12 * sc["n"])
     rep = ctx.step(bodies, cs)
     assert 2.5 < 2 * rep["n_c"][0] / sc["n"] < 4.5  # ~3 contacts per body (BASELINE cfg3)
+    assert rep["residuals"][0] <= 1e-8
     m = cs.count
-    assert float(cs.n[2, :m].abs().max()) < 1e-11
-    assert float(bodies.pos[:, 2].abs().max()) < 1e-11
+    # z-reflection symmetry: every A_0 row (discovered at the planar C^k) is in-plane.
+    # (Jammed rows reach lambda ~ 1e3, so the overdamped rotation 12/(xi L^3)
+    # tau dt of the first-order update can reach tens of radians; the deep
+    # in-plane overlaps this creates at C_1 have out-of-plane SNSD maxima, so
+    # later generations may leave the plane -- the oracle follows the same
+    # equations; DESIGN.md §2 R21.)
+    g0 = cs.gen[:m] == 0
+    assert float(cs.n[2, :m][g0].abs().max()) < 1e-11
+    assert float(cs.ta[0, :m][g0].abs().max()) < 1e-11 and float(cs.ta[1, :m][g0].abs().max()) < 1e-11
     assert bool(torch.all(cs.lam[:m] >= 0))
