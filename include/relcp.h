@@ -81,8 +81,15 @@ typedef struct relcp_params {
     double box[3];        /* periodic box lengths; 0 = that axis not periodic [0]  */
     double xi;            /* drag coefficient (overdamped) [1.0]          */
     int32_t n_dirs;       /* SNSD multistart sample size for overlaps [256] (R4)   */
-    int32_t reserved;
+    int32_t solver;       /* RELCP_SOLVER_BB [default] | RELCP_SOLVER_APGD         */
 } relcp_params;
+
+/* LCP solvers (the paper names only the family; reading R1):
+ *   BB   Barzilai-Borwein projected gradient (alternating BB1 / BB2 steps);
+ *   APGD Nesterov-accelerated projected gradient, step 1/(1.1 L), gradient
+ *        adaptive restart.  Same kernels and bytes per iteration (+2 vectors). */
+#define RELCP_SOLVER_BB 0
+#define RELCP_SOLVER_APGD 1
 
 /* Body view (SoA by field, each field row-major per body).
  *   pos         (n,3)  centre x_b                                  in/out (step)

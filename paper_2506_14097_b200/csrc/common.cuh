@@ -44,12 +44,14 @@ struct LcpState {
     double obj;     // x^T (g - q) = x^T A x
     double pnorm;   // power iteration: scale applied to the input vector
     double tol;
-    long long iter;     // completed BB iterations
+    long long iter;     // completed iterations
     long long max_iter;
     int done;
     int conv;
     int nan;
-    int pad;
+    int par;        // APGD: 0 -> (x, g) current, 1 -> (xb, gb) current
+    double theta;   // APGD momentum parameter
+    double beta;    // APGD extrapolation weight for the next step
 };
 
 // Per-body mobility block W_b in a single 7-double form, stored as 7 SoA
@@ -86,6 +88,7 @@ struct relcp_ctx {
     DevBuf<unsigned> counter;
     DevBuf<LcpState> st;
     DevBuf<double> vtmp;     // (nc) power iteration / apply scratch
+    DevBuf<double> apgd_buf; // (2, nc) APGD second iterate (x', g')
     LcpState *st_host = nullptr;  // pinned mirror
 
     // step state (from generate_contacts at C^k)
@@ -160,9 +163,11 @@ static inline int grid_for(int64_t n, int nt = RELCP_NT, int per_sm = 8) {
 // operator.cu
 int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *cs);
 int op_build_W(relcp_ctx *ctx, const relcp_bodies *b, double *W);
-// scatter (+ optional BB projection) followed by W: U = W D xeff
-int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int proj,
-               const double *xscale_dev, double *U, double *F);
+// scatter followed by W: U = W D x_eff; mode 0 x_eff = x, 1 BB projected step,
+// 2 APGD projected step from (x, g) / (xb, gb) (device parity picks current)
+int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int mode,
+               const double *xscale_dev, double *U, double *F, const double *xb = nullptr,
+               const double *gb = nullptr);
 int op_gather_apply(relcp_ctx *ctx, const relcp_constraints *cs, const double *U, double *y, double scale,
                     int norm2);
 int op_row_dot_U(relcp_ctx *ctx, const relcp_constraints *cs, int64_t begin, int64_t end, const double *U,

@@ -44,6 +44,9 @@ __global__ void k_state_init(LcpState *st, int64_t nc, double tol, long long max
     st->done = 0;
     st->conv = 0;
     st->nan = 0;
+    st->par = 0;
+    st->theta = 1.0;
+    st->beta = 0.0;
 }
 
 // g = s D^T U + q for the (projected) warm start; r_0; alpha_0 = 1/L.
@@ -151,6 +154,75 @@ __global__ void __launch_bounds__(RELCP_NT, ITER_MINB) k_lcp_iter(int64_t nc, in
     }
 }
 
+// APGD (NEXT rank 2): Nesterov-accelerated projected gradient with
+// gradient-based adaptive restart, in lagged form so that each iteration is
+// still one K6 + one K7 pass:
+//   y = x + beta (x - x'),  g_y = g + beta (g - g')        (linearity of A)
+//   x+ = max(0, y - t g_y),  g+ = A x+ + q                 (t = 1/(1.1 L))
+//   restart (theta = 1, beta = 0) if g_y . (x+ - x) > 0, else
+//   theta+ = (theta sqrt(theta^2 + 4) - theta^2) / 2,
+//   beta+  = theta (1 - theta) / (theta^2 + theta+).
+// The new iterate overwrites the previous one's slot; the parity bit flips.
+__global__ void __launch_bounds__(RELCP_NT, ITER_MINB) k_apgd_iter(
+    int64_t nc, int64_t cap, const int32_t *__restrict__ ia, const int32_t *__restrict__ ib,
+    const double *__restrict__ n, const double *__restrict__ ta, const double *__restrict__ tb,
+    const double *__restrict__ U, double s, const double *__restrict__ q, double *xA, double *gA, double *xB,
+    double *gB, double *part, unsigned *counter, LcpState *st) {
+    __shared__ double sh[3 * 32];
+    if (st->done) return;
+    const double t = st->alpha, beta = st->beta;
+    double *xc = xA, *gc = gA, *xp = xB, *gp = gB;
+    if (st->par) {
+        xc = xB; gc = gB; xp = xA; gp = gA;
+    }
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
+        const double x0 = xc[a], g0 = gc[a];
+        const double y = x0 + beta * (x0 - xp[a]), gy = g0 + beta * (g0 - gp[a]);
+        const double xn = fmax(0.0, y - t * gy);
+        const double gn = fma(s, row_dot_l(a, cap, ia, ib, n, ta, tb, U), q[a]);
+        xp[a] = xn;
+        gp[a] = gn;
+        acc[0] = fma(gy, xn - x0, acc[0]);
+        acc[1] = fmax(acc[1], fabs(fmin(xn, gn)));
+        acc[2] = fmax(acc[2], isfinite(gn) ? 0.0 : 1.0);
+    }
+    const int ops[3] = {0, 1, 1};
+    if (grid_reduce_last<3>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
+        const long long k = st->iter;
+        st->iter = k + 1;
+        st->par ^= 1;  // the new iterate is current
+        st->resid = acc[1];
+        if (acc[2] > 0.0 || !isfinite(acc[0])) {
+            st->nan = 1;
+            st->done = 1;
+            return;
+        }
+        if (acc[1] <= st->tol) {
+            st->conv = 1;
+            st->done = 1;
+            return;
+        }
+        const double th = st->theta;
+        if (acc[0] > 0.0) {  // adaptive restart
+            st->theta = 1.0;
+            st->beta = 0.0;
+        } else {
+            const double th1 = 0.5 * (th * sqrt(th * th + 4.0) - th * th);
+            st->beta = th * (1.0 - th) / (th * th + th1);
+            st->theta = th1;
+        }
+        if (k + 1 >= st->max_iter) st->done = 1;
+    }
+}
+
+__global__ void k_apgd_setup(LcpState *st) {
+    st->alpha = 1.0 / (1.1 * st->L);  // power iteration underestimates ||A|| slightly
+    st->theta = 1.0;
+    st->beta = 0.0;
+    st->par = 0;
+}
+
 // obj = x^T (g - q) = x^T A x
 __global__ void __launch_bounds__(RELCP_NT) k_objective(int64_t nc, const double *__restrict__ x,
                                                         const double *__restrict__ g, const double *__restrict__ q,
@@ -199,6 +271,18 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
     k_lcp_init<<<gridc, RELCP_NT, 0, st>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->U.p, s, cs->q,
                                            cs->lambda, cs->g, ctx->partials.p, ctx->counter.p, ctx->st.p);
     CKL();
+    const bool apgd = ctx->p.solver == RELCP_SOLVER_APGD;
+    double *xB = nullptr, *gB = nullptr;
+    if (apgd) {
+        // second iterate buffer (x', g') = (x_0, g_0); theta = 1, beta = 0, t = 1/(1.1 L)
+        CK(ctx->apgd_buf.grow(2 * nc));
+        xB = ctx->apgd_buf.p;
+        gB = ctx->apgd_buf.p + nc;
+        CK(cudaMemcpyAsync(xB, cs->lambda, sizeof(double) * nc, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(gB, cs->g, sizeof(double) * nc, cudaMemcpyDeviceToDevice, st));
+        k_apgd_setup<<<1, 1, 0, st>>>(ctx->st.p);
+        CKL();
+    }
     int batch = ctx->p.check_every > 0 ? ctx->p.check_every : 32;
     if (ctx->timing) {
         if (batch > 64) batch = 64;
@@ -215,11 +299,16 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
         for (int j = 0; j < batch; ++j) {
             // per-iteration events only in timing mode, which never captures graphs
             if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j], st));
-            CKS(op_scatter(ctx, nb, cs->lambda, cs->g, 1, nullptr, ctx->U.p, nullptr));
+            CKS(op_scatter(ctx, nb, cs->lambda, cs->g, apgd ? 2 : 1, nullptr, ctx->U.p, nullptr, xB, gB));
             if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j + 1], st));
-            k_lcp_iter<<<gridc, RELCP_NT, 0, st>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->U.p,
-                                                   s, cs->q, cs->lambda, cs->g, ctx->partials.p, ctx->counter.p,
-                                                   ctx->st.p);
+            if (apgd)
+                k_apgd_iter<<<gridc, RELCP_NT, 0, st>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb,
+                                                        ctx->U.p, s, cs->q, cs->lambda, cs->g, xB, gB,
+                                                        ctx->partials.p, ctx->counter.p, ctx->st.p);
+            else
+                k_lcp_iter<<<gridc, RELCP_NT, 0, st>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb,
+                                                       ctx->U.p, s, cs->q, cs->lambda, cs->g, ctx->partials.p,
+                                                       ctx->counter.p, ctx->st.p);
             CKL();
             if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j + 2], st));
         }
@@ -265,6 +354,10 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
         pending = batch;
     }
     if (gexec) CK(cudaGraphExecDestroy(gexec));
+    if (apgd && ctx->st_host->par) {  // the current APGD iterate lives in the second buffer
+        CK(cudaMemcpyAsync(cs->lambda, xB, sizeof(double) * nc, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(cs->g, gB, sizeof(double) * nc, cudaMemcpyDeviceToDevice, st));
+    }
     k_objective<<<gridc, RELCP_NT, 0, st>>>(nc, cs->lambda, cs->g, cs->q, ctx->partials.p, ctx->counter.p, ctx->st.p);
     CKL();
     CK(cudaMemcpyAsync(ctx->st_host, ctx->st.p, sizeof(LcpState), cudaMemcpyDeviceToHost, st));

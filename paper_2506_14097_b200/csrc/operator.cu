@@ -200,28 +200,47 @@ struct V6 {
 // the U / F transpose reuses a warp's staging area: 2 x 32 x 6 doubles
 static_assert(3 * (SCATTER_TILE + 1) * 2 >= 2 * 192, "SCATTER_TILE too small for the U/F staging");
 
-template <bool PROJ, bool SORTED>
+// MODE: 0 apply (x_eff = x), 1 BB step (x_eff = max(0, x - alpha g)),
+// 2 APGD step (y = x + beta (x - x'), g_y likewise, x_eff = max(0, y - t g_y);
+// (x, g) / (x', g') are (x, g) / (xb, gb) or swapped by the device parity bit).
+template <int MODE, bool SORTED>
 __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
     int64_t nb, int64_t E, const int *__restrict__ row_ptr, const int *__restrict__ ecid,
     const double *__restrict__ ew, const int *__restrict__ pa, int64_t cap, const double *__restrict__ cn,
     const double *__restrict__ cta, const double *__restrict__ x, const double *__restrict__ g,
-    const LcpState *__restrict__ st, const double *__restrict__ xscale, const double *__restrict__ W,
-    double *__restrict__ U, double *__restrict__ Fout) {
+    const double *__restrict__ xb, const double *__restrict__ gb, const LcpState *__restrict__ st,
+    const double *__restrict__ xscale, const double *__restrict__ W, double *__restrict__ U,
+    double *__restrict__ Fout) {
     // contributions staged as 3 planes of double2 (components 01, 23, 45):
     // 128-bit shared loads in the per-lane segment sums
     __shared__ double2 sm[SCATTER_WPB][3][SCATTER_TILE + 1];
-    double alpha = 0.0;
-    if (PROJ) {
+    double alpha = 0.0, beta = 0.0;
+    const double *xc = x, *gc = g, *xp = xb, *gp = gb;
+    if (MODE != 0) {
         if (st->done) return;
         alpha = st->alpha;
+    }
+    if (MODE == 2) {
+        beta = st->beta;
+        if (st->par) {
+            xc = xb; gc = gb; xp = x; gp = g;
+        }
     }
     const double sc = xscale ? *xscale : 1.0;
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     double2(*c6)[SCATTER_TILE + 1] = sm[wl];
     const int64_t nwarp = (nb + 31) >> 5;
     auto xeff = [&](int c) {
-        double xv = x[c];
-        if (PROJ) xv = fmax(0.0, xv - alpha * g[c]);
+        double xv;
+        if (MODE == 0) {
+            xv = xc[c];
+        } else if (MODE == 1) {
+            xv = fmax(0.0, xc[c] - alpha * gc[c]);
+        } else {
+            const double x0 = xc[c], g0 = gc[c];
+            const double y = x0 + beta * (x0 - xp[c]), gy = g0 + beta * (g0 - gp[c]);
+            xv = fmax(0.0, y - alpha * gy);
+        }
         return xv * sc;
     };
     for (int64_t w = blockIdx.x * (int64_t)SCATTER_WPB + wl; w < nwarp; w += (int64_t)gridDim.x * SCATTER_WPB) {
@@ -309,8 +328,8 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
     }
 }
 
-int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int proj, const double *xscale_dev,
-               double *U, double *F) {
+int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int mode, const double *xscale_dev,
+               double *U, double *F, const double *xb, const double *gb) {
     const int64_t E = ctx->op_sorted ? ctx->op_nc : 2 * ctx->op_nc;
     const int64_t nwarp = (nb + 31) / 32;
     int64_t grid = (nwarp + SCATTER_WPB - 1) / SCATTER_WPB;
@@ -320,14 +339,16 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
     const int *pa = ctx->pa.p;
     const int64_t cap = ctx->op_cap;
     const double *cn = ctx->op_n, *cta = ctx->op_ta;
-#define SCATTER_ARGS nb, E, ctx->row_ptr.p, ctx->ecid.p, ctx->ew.p, pa, cap, cn, cta, x, g, ctx->st.p, xscale_dev, \
-                     ctx->W.p, U, F
+#define SCATTER_ARGS nb, E, ctx->row_ptr.p, ctx->ecid.p, ctx->ew.p, pa, cap, cn, cta, x, g, xb, gb, ctx->st.p, \
+                     xscale_dev, ctx->W.p, U, F
     if (ctx->op_sorted) {
-        if (proj) k_scatter<true, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
-        else k_scatter<false, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+        if (mode == 1) k_scatter<1, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+        else if (mode == 2) k_scatter<2, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+        else k_scatter<0, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
     } else {
-        if (proj) k_scatter<true, false><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
-        else k_scatter<false, false><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+        if (mode == 1) k_scatter<1, false><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+        else if (mode == 2) k_scatter<2, false><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+        else k_scatter<0, false><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
     }
 #undef SCATTER_ARGS
     CKL();
