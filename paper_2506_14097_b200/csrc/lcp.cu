@@ -20,6 +20,9 @@
 #ifndef ITER_MINB
 #define ITER_MINB 4  // resident K7 blocks per SM (register budget); grid = 148 * ITER_MINB
 #endif
+#ifndef ITER_ILP
+#define ITER_ILP 2   // rows per thread per trip in K7
+#endif
 
 __global__ void k_project(int64_t nc, double *x) {
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x)
@@ -97,11 +100,11 @@ __global__ void __launch_bounds__(RELCP_NT, ITER_MINB) k_lcp_iter(int64_t nc, in
     const double alpha = st->alpha;
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    // two constraints per thread per trip: independent loads in flight (ILP)
-    for (int64_t a0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a0 < nc; a0 += 2 * stride) {
-        double xo[2], go[2], qv[2], rd[2];
+    // ITER_ILP constraints per thread per trip: independent loads in flight (ILP)
+    for (int64_t a0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a0 < nc; a0 += ITER_ILP * stride) {
+        double xo[ITER_ILP], go[ITER_ILP], qv[ITER_ILP], rd[ITER_ILP];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < ITER_ILP; ++u) {
             const int64_t a = a0 + u * stride;
             const bool ok = a < nc;
             const int64_t ac = ok ? a : a0;
@@ -111,7 +114,7 @@ __global__ void __launch_bounds__(RELCP_NT, ITER_MINB) k_lcp_iter(int64_t nc, in
             rd[u] = row_dot_l(ac, cap, ia, ib, n, ta, tb, U);
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < ITER_ILP; ++u) {
             const int64_t a = a0 + u * stride;
             if (a >= nc) continue;
             const double xn = fmax(0.0, xo[u] - alpha * go[u]);

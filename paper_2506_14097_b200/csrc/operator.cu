@@ -358,6 +358,9 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
 // ------------------------------------------------------------ gather
 #include "rows.cuh"
 #define row_dot row_dot_u
+#ifndef GATHER_ILP
+#define GATHER_ILP 4  // rows per thread per trip in the apply gather (independent loads in flight)
+#endif
 
 // y = scale * D^T U ; optionally the grid-wide ||y||^2 -> st->pnorm = 1/||y||, st->L = ||y||
 __global__ void __launch_bounds__(RELCP_NT) k_gather(int64_t nc, int64_t cap, const int32_t *__restrict__ ia,
@@ -369,15 +372,15 @@ __global__ void __launch_bounds__(RELCP_NT) k_gather(int64_t nc, int64_t cap, co
     __shared__ double sh[32];
     double acc[1] = {0.0};
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t a0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a0 < nc; a0 += 2 * stride) {
-        double v[2];
+    for (int64_t a0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a0 < nc; a0 += GATHER_ILP * stride) {
+        double v[GATHER_ILP];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < GATHER_ILP; ++u) {
             const int64_t a = a0 + u * stride;
             v[u] = scale * row_dot(a < nc ? a : a0, cap, ia, ib, n, ta, tb, U);
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < GATHER_ILP; ++u) {
             const int64_t a = a0 + u * stride;
             if (a >= nc) continue;
             y[a] = v[u];
