@@ -136,6 +136,19 @@ class Clocks:
 
 
 # ---------------------------------------------------------------- ours
+def combine_ranks(ms, iters, dist, device):
+    """Whole-job aggregate over replicas: the MAX device time over ranks and
+    the SUM of the iterations every rank executed (value = sum / max)."""
+    if not dist:
+        return ms, float(iters)
+    import torch
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    it_t = torch.tensor([float(iters)], dtype=torch.float64, device=device)
+    dist.all_reduce(it_t, op=dist.ReduceOp.SUM)
+    return float(t.item()), float(it_t.item())
+
+
 def iter_bytes(n_c, iters, n):
     return sum(it * (216.0 * c + 152.0 * n) for c, it in zip(n_c, iters))
 
@@ -197,16 +210,7 @@ def run_ours(args, rank, world, dist):
     assert iters == stats["lcp_iterations"], (iters, stats)
     nbytes = sum(iter_bytes(r["n_c"], r["iterations"], args.n) for r in reports)
     it_ms = stats["scatter_ms"] + stats["gather_ms"]
-    # max over ranks of the time, sum of the iterations
-    if dist:
-        import torch.distributed as tdist
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        it_t = torch.tensor([float(iters)], dtype=torch.float64, device=dev)
-        tdist.all_reduce(it_t, op=tdist.ReduceOp.SUM)
-        ms_max, iters_all = float(t.item()), float(it_t.item())
-    else:
-        ms_max, iters_all = ms, float(iters)
+    ms_max, iters_all = combine_ranks(ms, iters, dist, dev)
     value = iters_all / (ms_max / 1e3)
 
     peaks = {}
