@@ -28,6 +28,9 @@
 #ifndef SCATTER_TILE
 #define SCATTER_TILE 64  // entries staged per warp per tile
 #endif
+#ifndef K6_REVERSE
+#define K6_REVERSE 1
+#endif
 #ifndef SCATTER_MINB
 #define SCATTER_MINB 8   // resident blocks per SM the register budget must allow (64 regs at 4 warps)
 #endif
@@ -243,7 +246,11 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
         }
         return xv * sc;
     };
-    for (int64_t w = blockIdx.x * (int64_t)SCATTER_WPB + wl; w < nwarp; w += (int64_t)gridDim.x * SCATTER_WPB) {
+    for (int64_t wi = blockIdx.x * (int64_t)SCATTER_WPB + wl; wi < nwarp; wi += (int64_t)gridDim.x * SCATTER_WPB) {
+        // K6_REVERSE: sweep bodies high -> low, so K6 starts on the rows, x and g
+        // K7 (ascending) touched last (still in L2) and ends on the bodies whose
+        // U / rows K7 touches first
+        const int64_t w = K6_REVERSE ? nwarp - 1 - wi : wi;
         const int64_t b0 = w << 5;
         const int64_t b = b0 + lane;
         const bool own = b < nb;
