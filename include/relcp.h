@@ -87,9 +87,15 @@ typedef struct relcp_params {
 /* LCP solvers (the paper names only the family; reading R1):
  *   BB   Barzilai-Borwein projected gradient (alternating BB1 / BB2 steps);
  *   APGD Nesterov-accelerated projected gradient, step 1/(1.1 L), gradient
- *        adaptive restart.  Same kernels and bytes per iteration (+2 vectors). */
+ *        adaptive restart.  Same kernels and bytes per iteration (+2 vectors).
+ *   APGD_FUSED  the same APGD iterates with one fewer pass over the a-side
+ *        rows: the row pass also takes the projected step and forms the
+ *        a-side wrench sums of the next iterate, the scatter adds the b-side
+ *        (fewer bytes per iteration).  Needs the library's sorted store order
+ *        (plain APGD otherwise). */
 #define RELCP_SOLVER_BB 0
 #define RELCP_SOLVER_APGD 1
+#define RELCP_SOLVER_APGD_FUSED 2
 
 /* Body view (SoA by field, each field row-major per body).
  *   pos         (n,3)  centre x_b                                  in/out (step)

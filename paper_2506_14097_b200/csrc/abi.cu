@@ -28,7 +28,8 @@ static int check_params(const relcp_params *p) {
     for (int k = 0; k < 3; ++k)
         if (!(p->box[k] >= 0.0)) return 0;
     if (p->dynamics == RELCP_OVERDAMPED && !(p->xi > 0.0)) return 0;
-    if (p->solver != RELCP_SOLVER_BB && p->solver != RELCP_SOLVER_APGD) return 0;
+    if (p->solver != RELCP_SOLVER_BB && p->solver != RELCP_SOLVER_APGD && p->solver != RELCP_SOLVER_APGD_FUSED)
+        return 0;
     return 1;
 }
 

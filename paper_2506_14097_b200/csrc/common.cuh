@@ -52,6 +52,7 @@ struct LcpState {
     int par;        // APGD: 0 -> (x, g) current, 1 -> (xb, gb) current
     double theta;   // APGD momentum parameter
     double beta;    // APGD extrapolation weight for the next step
+    double alpha_next;  // fused BB: step of the pass after the next (one-step delay)
 };
 
 // Per-body mobility block W_b in a single 7-double form, stored as 7 SoA
@@ -88,7 +89,8 @@ struct relcp_ctx {
     DevBuf<unsigned> counter;
     DevBuf<LcpState> st;
     DevBuf<double> vtmp;     // (nc) power iteration / apply scratch
-    DevBuf<double> apgd_buf; // (2, nc) APGD second iterate (x', g')
+    DevBuf<double> apgd_buf; // (2, nc) APGD second iterate (x', g'); fused BB: x'
+    DevBuf<double> Fa;       // (6, nb) fused BB: a-side wrench sums of the next iterate
     LcpState *st_host = nullptr;  // pinned mirror
 
     // step state (from generate_contacts at C^k)
@@ -170,7 +172,8 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
                const double *gb = nullptr);
 int op_gather_apply(relcp_ctx *ctx, const relcp_constraints *cs, const double *U, double *y, double scale,
                     int norm2);
-int op_row_dot_U(relcp_ctx *ctx, const relcp_constraints *cs, int64_t begin, int64_t end, const double *U,
+// fused BB row pass (g_{k+1}, x_{k+2}, a-side sums Fa, BB reductions)
+int op_fused_rows(relcp_ctx *ctx, const relcp_constraints *cs, int64_t nb, double s, double *xA, double *xB);int op_row_dot_U(relcp_ctx *ctx, const relcp_constraints *cs, int64_t begin, int64_t end, const double *U,
                  double coef, double *out_add);
 // store.cu
 int store_merge_appended(relcp_ctx *ctx, relcp_constraints *cs, int64_t n_old, int64_t m);

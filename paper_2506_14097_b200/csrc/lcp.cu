@@ -274,8 +274,19 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
     k_lcp_init<<<gridc, RELCP_NT, 0, st>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->U.p, s, cs->q,
                                            cs->lambda, cs->g, ctx->partials.p, ctx->counter.p, ctx->st.p);
     CKL();
-    const bool apgd = ctx->p.solver == RELCP_SOLVER_APGD;
+    const bool apgd = ctx->p.solver == RELCP_SOLVER_APGD || (ctx->p.solver == RELCP_SOLVER_APGD_FUSED && !ctx->op_sorted);
+    // fused APGD needs the sorted store (a-side rows contiguous); else plain APGD
+    const bool fused = ctx->p.solver == RELCP_SOLVER_APGD_FUSED && ctx->op_sorted;
     double *xB = nullptr, *gB = nullptr;
+    if (fused) {
+        // second iterate slot x_{-1} = x_0 (beta_0 = 0 makes it irrelevant but
+        // finite); theta = 1, beta = 0, t = 1/(1.1 L); U = W D x_0 is current
+        CK(ctx->apgd_buf.grow(nc));
+        xB = ctx->apgd_buf.p;
+        CK(cudaMemcpyAsync(xB, cs->lambda, sizeof(double) * nc, cudaMemcpyDeviceToDevice, st));
+        k_apgd_setup<<<1, 1, 0, st>>>(ctx->st.p);
+        CKL();
+    }
     if (apgd) {
         // second iterate buffer (x', g') = (x_0, g_0); theta = 1, beta = 0, t = 1/(1.1 L)
         CK(ctx->apgd_buf.grow(2 * nc));
@@ -301,6 +312,15 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
     auto enqueue_batch = [&]() -> int {
         for (int j = 0; j < batch; ++j) {
             // per-iteration events only in timing mode, which never captures graphs
+            if (fused) {
+                // row pass (g_{k+1}, x_{k+2}, a-side sums) then the b-side scatter + W
+                if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j], st));
+                CKS(op_fused_rows(ctx, cs, nb, s, cs->lambda, xB));
+                if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j + 1], st));
+                CKS(op_scatter(ctx, nb, cs->lambda, nullptr, 3, nullptr, ctx->U.p, nullptr, xB, nullptr));
+                if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j + 2], st));
+                continue;
+            }
             if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j], st));
             CKS(op_scatter(ctx, nb, cs->lambda, cs->g, apgd ? 2 : 1, nullptr, ctx->U.p, nullptr, xB, gB));
             if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j + 1], st));
@@ -361,6 +381,8 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
         CK(cudaMemcpyAsync(cs->lambda, xB, sizeof(double) * nc, cudaMemcpyDeviceToDevice, st));
         CK(cudaMemcpyAsync(cs->g, gB, sizeof(double) * nc, cudaMemcpyDeviceToDevice, st));
     }
+    if (fused && ctx->st_host->par)  // the current fused-BB iterate lives in the second slot
+        CK(cudaMemcpyAsync(cs->lambda, xB, sizeof(double) * nc, cudaMemcpyDeviceToDevice, st));
     k_objective<<<gridc, RELCP_NT, 0, st>>>(nc, cs->lambda, cs->g, cs->q, ctx->partials.p, ctx->counter.p, ctx->st.p);
     CKL();
     CK(cudaMemcpyAsync(ctx->st_host, ctx->st.p, sizeof(LcpState), cudaMemcpyDeviceToHost, st));

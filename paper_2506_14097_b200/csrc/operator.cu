@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
     const double *__restrict__ cta, const double *__restrict__ x, const double *__restrict__ g,
     const double *__restrict__ xb, const double *__restrict__ gb, const LcpState *__restrict__ st,
     const double *__restrict__ xscale, const double *__restrict__ W, double *__restrict__ U,
-    double *__restrict__ Fout) {
+    double *__restrict__ Fout, const double *__restrict__ Fa) {
     // contributions staged as 3 planes of double2 (components 01, 23, 45):
     // 128-bit shared loads in the per-lane segment sums
     __shared__ double2 sm[SCATTER_WPB][3][SCATTER_TILE + 1];
@@ -229,13 +229,14 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
             xc = xb; gc = gb; xp = x; gp = g;
         }
     }
+    if (MODE == 3 && st->par) xc = xb;  // fused BB: current iterate slot
     const double sc = xscale ? *xscale : 1.0;
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     double2(*c6)[SCATTER_TILE + 1] = sm[wl];
     const int64_t nwarp = (nb + 31) >> 5;
     auto xeff = [&](int c) {
         double xv;
-        if (MODE == 0) {
+        if (MODE == 0 || MODE == 3) {
             xv = xc[c];
         } else if (MODE == 1) {
             xv = fmax(0.0, xc[c] - alpha * gc[c]);
@@ -282,7 +283,12 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
                 __syncwarp();
             }
         };
-        if (SORTED) {
+        if (MODE == 3) {
+            // a-side sums were formed by the fused row pass (k_fused_rows)
+            if (own)
+#pragma unroll
+                for (int k = 0; k < 6; ++k) f[k] = Fa[k * nb + b];
+        } else if (SORTED) {
             const int sa = own ? pa[b] : 0, ta_ = own ? pa[b + 1] : 0;
             tiles(sa, ta_, [&](int e) {
                 const double xv = xeff(e);
@@ -347,8 +353,11 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
     const int64_t cap = ctx->op_cap;
     const double *cn = ctx->op_n, *cta = ctx->op_ta;
 #define SCATTER_ARGS nb, E, ctx->row_ptr.p, ctx->ecid.p, ctx->ew.p, pa, cap, cn, cta, x, g, xb, gb, ctx->st.p, \
-                     xscale_dev, ctx->W.p, U, F
-    if (ctx->op_sorted) {
+                     xscale_dev, ctx->W.p, U, F, ctx->Fa.p
+    if (mode == 3) {
+        if (!ctx->op_sorted) return set_err(ctx, RELCP_E_STATE, "fused solver needs a store sorted by ia");
+        k_scatter<3, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+    } else if (ctx->op_sorted) {
         if (mode == 1) k_scatter<1, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
         else if (mode == 2) k_scatter<2, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
         else k_scatter<0, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
@@ -362,9 +371,133 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
     return RELCP_OK;
 }
 
-// ------------------------------------------------------------ gather
+// ------------------------------------------------------------ fused BB row pass
 #include "rows.cuh"
 #define row_dot row_dot_u
+
+// Fused APGD iteration (solver RELCP_SOLVER_APGD_FUSED), row pass of iteration k.
+// APGD's extrapolation weight beta_k is fixed by the previous pass's restart
+// test, so every row can finish, from data already in registers,
+//   g_k = A x_k + q,  y = x_k + beta (x_k - x_{k-1}),  g_y = g_k + beta (g_k - g_{k-1}),
+//   x_{k+1} = max(0, y - t g_y)   and the restart dot g_y . (x_{k+1} - x_k),
+// AND form the a-side wrench sums of x_{k+1} (K6's a-side re-read of the rows
+// disappears; K6 mode 3 adds the b-side).  Same iterates as solver APGD up to
+// rounding.  Body-major over the sorted store: warp = 32 bodies, their a-side
+// rows are one contiguous range, streamed in coalesced tiles; shared-memory
+// segment sums (fixed order).
+//   in : x_k (cur slot), x_{k-1} (prev slot), g_{k-1} (g), U = W D x_k
+//   out: g_k (g, in place), x_{k+1} (prev slot), Fa = a-side sums of x_{k+1}
+#ifndef FUSED_MINB
+#define FUSED_MINB 5  // register budget ~100 (the row work + staging would spill at 64)
+#endif
+__global__ void __launch_bounds__(32 * SCATTER_WPB, FUSED_MINB) k_fused_rows(
+    int64_t nb, int64_t cap, const int *__restrict__ pa, const int32_t *__restrict__ ia,
+    const int32_t *__restrict__ ib, const double *__restrict__ n, const double *__restrict__ ta,
+    const double *__restrict__ tb, const double *__restrict__ U, double s, const double *__restrict__ q,
+    double *xA, double *xB, double *g, double *__restrict__ Fa, double *part, unsigned *counter, LcpState *st) {
+    __shared__ double2 sm[SCATTER_WPB][3][SCATTER_TILE + 1];
+    __shared__ double shr[3 * 32];
+    if (st->done) return;
+    const double t = st->alpha, beta = st->beta;
+    double *xc = xA, *xp = xB;
+    if (st->par) {
+        xc = xB; xp = xA;
+    }
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    double2(*c6)[SCATTER_TILE + 1] = sm[wl];
+    const int64_t nwarp = (nb + 31) >> 5;
+    double acc[3] = {0.0, 0.0, 0.0};  // restart dot, residual, non-finite flag
+    for (int64_t w = blockIdx.x * (int64_t)SCATTER_WPB + wl; w < nwarp; w += (int64_t)gridDim.x * SCATTER_WPB) {
+        const int64_t b0 = w << 5;
+        const int64_t b = b0 + lane;
+        const bool own = b < nb;
+        const int last = nb - b0 < 32 ? (int)(nb - b0 - 1) : 31;
+        const int sa = own ? pa[b] : 0, tA = own ? pa[b + 1] : 0;
+        const int e0 = __shfl_sync(0xffffffffu, sa, 0);
+        const int e1 = __shfl_sync(0xffffffffu, tA, last);
+        double f[6] = {0, 0, 0, 0, 0, 0};
+        for (int base = e0; base < e1; base += SCATTER_TILE) {
+#pragma unroll
+            for (int i = 0; i < SCATTER_TILE / 32; ++i) {
+                const int e = base + lane + 32 * i;
+                if (e < e1) {
+                    const double x1 = xc[e], x0 = xp[e], g0 = g[e];  // x_k, x_{k-1}, g_{k-1}
+                    const double g1 = fma(s, row_dot(e, cap, ia, ib, n, ta, tb, U), q[e]);  // g_k
+                    const double y = x1 + beta * (x1 - x0), gy = g1 + beta * (g1 - g0);
+                    const double x2 = fmax(0.0, y - t * gy);  // x_{k+1}
+                    xp[e] = x2;
+                    g[e] = g1;
+                    acc[0] = fma(gy, x2 - x1, acc[0]);
+                    acc[1] = fmax(acc[1], fabs(fmin(x1, g1)));
+                    acc[2] = fmax(acc[2], isfinite(g1) ? 0.0 : 1.0);
+                    const double nx = n[e], ny = n[cap + e], nz = n[2 * cap + e];
+                    const double tx = ta[e], ty = ta[cap + e], tz = ta[2 * cap + e];
+                    c6[0][lane + 32 * i] = make_double2(-nx * x2, -ny * x2);
+                    c6[1][lane + 32 * i] = make_double2(-nz * x2, -tx * x2);
+                    c6[2][lane + 32 * i] = make_double2(-ty * x2, -tz * x2);
+                }
+            }
+            __syncwarp();
+            const int lo = max(sa, base) - base, hi = min(tA, base + SCATTER_TILE) - base;
+            for (int j = lo; j < hi; ++j)
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const double2 c = c6[k][j];
+                    f[2 * k] += c.x;
+                    f[2 * k + 1] += c.y;
+                }
+            __syncwarp();
+        }
+        if (own)
+#pragma unroll
+            for (int k = 0; k < 6; ++k) Fa[k * nb + b] = f[k];
+    }
+    const int ops[3] = {0, 1, 1};
+    if (grid_reduce_last<3>(acc, ops, part, counter, shr) && threadIdx.x == 0) {
+        const long long k = st->iter;
+        st->resid = acc[1];  // residual of (x_k, g_k)
+        if (acc[2] > 0.0 || !isfinite(acc[0])) {
+            st->nan = 1;
+            st->done = 1;
+            return;
+        }
+        if (acc[1] <= st->tol) {  // (x_k, g_k) solve the LCP: x_k stays current
+            st->conv = 1;
+            st->done = 1;
+            return;
+        }
+        if (k >= st->max_iter) {  // stop on the consistent pair (x_k, g_k)
+            st->done = 1;
+            return;
+        }
+        st->iter = k + 1;
+        const double th = st->theta;
+        if (acc[0] > 0.0) {  // adaptive restart
+            st->theta = 1.0;
+            st->beta = 0.0;
+        } else {
+            const double th1 = 0.5 * (th * sqrt(th * th + 4.0) - th * th);
+            st->beta = th * (1.0 - th) / (th * th + th1);
+            st->theta = th1;
+        }
+        st->par ^= 1;  // x_{k+1} becomes current
+    }
+}
+
+int op_fused_rows(relcp_ctx *ctx, const relcp_constraints *cs, int64_t nb, double s, double *xA, double *xB) {
+    CK(ctx->Fa.grow(6 * nb));
+    const int64_t nwarp = (nb + 31) / 32;
+    int64_t grid = (nwarp + SCATTER_WPB - 1) / SCATTER_WPB;
+    if (grid > (int64_t)RELCP_SM_COUNT * FUSED_MINB) grid = (int64_t)RELCP_SM_COUNT * FUSED_MINB;
+    if (grid < 1) grid = 1;
+    k_fused_rows<<<(unsigned)grid, 32 * SCATTER_WPB, 0, ctx->stream>>>(
+        nb, cs->capacity, ctx->pa.p, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->U.p, s, cs->q, xA, xB, cs->g,
+        ctx->Fa.p, ctx->partials.p, ctx->counter.p, ctx->st.p);
+    CKL();
+    return RELCP_OK;
+}
+
+// ------------------------------------------------------------ gather
 #ifndef GATHER_ILP
 #define GATHER_ILP 4  // rows per thread per trip in the apply gather (independent loads in flight)
 #endif

@@ -38,7 +38,7 @@ class Params(ctypes.Structure):
                 ("box", f64 * 3), ("xi", f64), ("n_dirs", i32), ("solver", i32)]
 
 
-SOLVER_BB, SOLVER_APGD = 0, 1
+SOLVER_BB, SOLVER_APGD, SOLVER_APGD_FUSED = 0, 1, 2
 
 
 class Bodies(ctypes.Structure):

@@ -101,7 +101,7 @@ def cfg1_a0(orc):
     return sc, r
 
 
-@pytest.mark.parametrize("solver", [0, 1])
+@pytest.mark.parametrize("solver", [0, 1, 2])
 def test_lcp_solve_parity_cfg1(orc, R, cfg1_a0, solver):
     sc, r = cfg1_a0
     c = r["constraints"]
@@ -127,7 +127,7 @@ def test_lcp_solve_parity_cfg1(orc, R, cfg1_a0, solver):
     assert abs(rep["objective"] - r["f"][0]) <= 1e-6 * abs(r["f"][0])
 
 
-@pytest.mark.parametrize("solver", [0, 1])
+@pytest.mark.parametrize("solver", [0, 1, 2])
 @pytest.mark.parametrize("seed", [0, 1, 2])
 def test_lcp_vs_enumeration_tiny(orc, R, seed, solver):
     """Tiny random LCPs: the GPU solution equals the brute-force support
@@ -342,7 +342,7 @@ def test_step_deterministic(R):
 
 # ------------------------------------------------------------ cfg3 / cfg4 recipes
 
-@pytest.mark.parametrize("solver", [0, 1])
+@pytest.mark.parametrize("solver", [0, 1, 2])
 @pytest.mark.parametrize("c_fixed", [None, 3])
 def test_cfg4_network_lcp_parity(orc, R, c_fixed, solver):
     """Given chainmail network (cfg4 recipe, 16 x 16 rings): rows, q, and the

@@ -14,7 +14,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 2_000_000
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 sc = scenes.cfg5(n=n)
 ctx = R.Context(dynamics=sc["dynamics"], dt=sc["dt"], box=list(sc["box"]), lcp_max_iter=iters, lcp_tol=1e-30,
-                power_iters=2)
+                solver=int(os.environ.get("RELCP_SOLVER", "0")))  # 20 power iterations: APGD steps 1/(1.1 L)
 bodies = R.BodyState.from_scene(sc)
 cs = R.ConstraintStore(8 * n)
 ctx.generate_contacts(bodies, cs)

@@ -20,7 +20,7 @@ for name, mk, rec in cases:
     if sel and name not in sel:
         continue
     sc = mk()
-    for solver in (0, 1):
+    for solver in (0, 1, 2):
         ctx = R.Context(dynamics=sc["dynamics"], dt=sc["dt"], box=list(sc["box"]), lcp_tol=1e-8,
                         lcp_max_iter=30000, max_recursions=rec, solver=solver)
         bodies = R.BodyState.from_scene(sc)
@@ -36,5 +36,5 @@ for name, mk, rec in cases:
             rep = ctx.step(bodies, cs)
             out = {k: rep[k] for k in ("iterations", "residuals", "n_c", "recursions", "max_overlap")}
         torch.cuda.synchronize()
-        out.update(config=name, solver=["BB", "APGD"][solver], seconds=time.time() - t)
+        out.update(config=name, solver=["BB", "APGD", "APGD_FUSED"][solver], seconds=time.time() - t)
         print(json.dumps(out), flush=True)
