@@ -128,8 +128,18 @@ def cfg5(seed: int = 5, n: int = 2_000_000) -> dict:
                       dynamics=INERTIAL, name="cfg5" if n == 2_000_000 else f"cfg5-n{n}")
 
 
+def colony_rods(seed: int = 7, n: int = 131_072, dt: float = 1e-2, patch: int = 6) -> dict:
+    """The paper's colony shape class: spherocylinders
+    of diameter b = 0.5 and centreline length l ~ U(2, 4) (between l_0 and the
+    division length 2 l_0), planar, packed with the cfg3 row-patch
+    construction, every cell grown by l <- l e^dt (l_dot = l) at the start of
+    the step; 2^17 cells by default.  Overdamped local drag with L = l + b
+    (R22).  Division is out of scope."""
+    return cfg3(seed=seed, n=n, patch=patch, rods=True, dt=dt)
+
+
 def cfg3(seed: int = 3, n: int = 200_000, patch: int = 6, gap: float = 0.005, minor: float = 0.25,
-         growth: float = 0.01, dt: float = 1e-2) -> dict:
+         growth: float = 0.01, dt: float = 1e-2, rods: bool = False) -> dict:
     """Growing-colony-like monolayer (BASELINE cfg3, SURVEY §8(d) row-patch
     construction): ellipsoids (a, 0.25, 0.25), a ~ U(0.5, 1.0), centres in
     z = 0, symmetry axis in-plane.  P x P square patches, each with a director
@@ -145,9 +155,12 @@ def cfg3(seed: int = 3, n: int = 200_000, patch: int = 6, gap: float = 0.005, mi
     dt = 1e-2, no external force, non-periodic.  Draw order: a per site, patch
     directors, row offsets, growth set."""
     rng = np.random.Generator(np.random.PCG64(seed))
-    # disk radius from the realised packing (~0.6 area fraction of a ~ 0.75 x 0.25 ellipses)
-    area_body = math.pi * 0.75 * minor
-    radius = math.sqrt(n * area_body / 0.55 / math.pi) + 4.0
+    # tip half-length law: ellipsoid a ~ U(0.5, 1); rod (l + b)/2 with l ~ U(2, 4)
+    a_lo, a_hi = (0.5, 1.0) if not rods else (1.0 + minor, 2.0 + minor)
+    # disk radius from the realised packing (~0.55 area fraction)
+    area_body = math.pi * 0.5 * (a_lo + a_hi) * minor
+    fill, rim = (0.55, 4.0) if not rods else (0.40, 3.0 * a_hi)  # long rods lose more at patch borders
+    radius = math.sqrt(n * area_body / fill / math.pi) + rim
     side = 2.0 * radius
     psz = side / patch
     theta = rng.uniform(0.0, math.pi, size=(patch, patch))
@@ -163,7 +176,7 @@ def cfg3(seed: int = 3, n: int = 200_000, patch: int = 6, gap: float = 0.005, mi
             for rv in rows:
                 t = -half + rng.uniform(0.0, 1.0)
                 while t < half:
-                    a = rng.uniform(0.5, 1.0)
+                    a = rng.uniform(a_lo, a_hi)
                     c = np.array([cx, cy]) + (t + a) * u + rv * v
                     t += 2 * a + gap
                     if abs(c[0] - cx) > psz / 2 or abs(c[1] - cy) > psz / 2:
@@ -180,7 +193,7 @@ def cfg3(seed: int = 3, n: int = 200_000, patch: int = 6, gap: float = 0.005, mi
     owner = np.array(owner)
     # greedy cross-patch rejection with bounding circles (grid hashing)
     keep = np.ones(len(pts), dtype=bool)
-    cell = 2.0
+    cell = 2.0 * a_hi  # +-1 cells must reach the largest a_i + a_j
     grid = {}
     for i in range(len(pts)):
         gx, gy = int(math.floor(pts[i, 0] / cell)), int(math.floor(pts[i, 1] / cell))
@@ -210,19 +223,30 @@ def cfg3(seed: int = 3, n: int = 200_000, patch: int = 6, gap: float = 0.005, mi
     pts, angs, majors = pts[order], angs[order], majors[order]
     grow = np.zeros(n, dtype=bool)
     grow[rng.permutation(n)[: n // 2]] = True
-    majors = majors + growth * grow
     pos = np.zeros((n, 3))
     pos[:, :2] = pts
     quat = np.zeros((n, 4))
     quat[:, 0] = np.cos(angs / 2)
     quat[:, 3] = np.sin(angs / 2)
-    axes = np.stack([majors, np.full(n, minor), np.full(n, minor)], axis=1)
-    inv_mass, inv_inertia = _ellipsoid_mass_props(axes)
-    return dict(name="cfg3" if n == 200_000 else f"cfg3-n{n}", n=n, pos=pos, quat=quat, axes=axes,
+    if rods:
+        # spherocylinder: axes = (l/2, r, r); every cell grows l <- l e^dt
+        ell = 2.0 * (majors - minor) * math.exp(dt)
+        axes = np.stack([0.5 * ell, np.full(n, minor), np.full(n, minor)], axis=1)
+        shape = np.ones(n, dtype=np.int32)
+        grow[:] = True
+        area = (ell * 2 * minor + math.pi * minor ** 2).sum()
+    else:
+        majors = majors + growth * grow
+        axes = np.stack([majors, np.full(n, minor), np.full(n, minor)], axis=1)
+        shape = np.zeros(n, dtype=np.int32)
+        area = math.pi * (axes[:, 0] * axes[:, 1]).sum()
+    inv_mass, inv_inertia = _ellipsoid_mass_props(axes)  # unused: overdamped dynamics
+    name = ("rods" if rods else "cfg3") + ("" if n == (131_072 if rods else 200_000) else f"-n{n}")
+    return dict(name=name, n=n, pos=pos, quat=quat, axes=axes, shape=shape,
                 vel=np.zeros((n, 6)), inv_mass=inv_mass, inv_inertia=inv_inertia,
                 kinematic=np.zeros(n, dtype=np.int32), box=np.zeros(3), dt=float(dt), dynamics=OVERDAMPED,
                 xi=1.0, cutoff=0.1, eps_ncp=1e-5, lcp_tol=1e-8, seed=seed, growing=grow,
-                area_fraction=float((axes[:, 0] * axes[:, 1]).sum() / (pts ** 2).sum(1).max()))
+                area_fraction=float(area / (math.pi * (pts ** 2).sum(1).max())))
 
 
 def cfg4(seed: int = 4, n_side: int = 1000, R: float = 1.0, r: float = 0.2, pitch: float = 1.4,

@@ -105,7 +105,15 @@ typedef struct relcp_params {
  *                      overdamped bodies                           in/out (step)
  *   inv_mass    (n)    1/m   (inertial; may be NULL if overdamped) in
  *   inv_inertia (n,3)  1/I_k, principal body-frame (inertial)      in
- *   kinematic   (n) int32, 1 = prescribed velocity (W_b = 0); NULL = none */
+ *   kinematic   (n) int32, 1 = prescribed velocity (W_b = 0); NULL = none
+ *   shape       (n) int32, RELCP_SHAPE_ELLIPSOID (axes = semi-axes) or
+ *               RELCP_SHAPE_SPHEROCYLINDER (axes[0] = half the centreline
+ *               length l/2 along body x, axes[1] = cap radius r; SNSD =
+ *               segment distance minus radii; drag length l + 2r);
+ *               NULL = all ellipsoids.  Mixed ellipsoid-rod pairs are not
+ *               defined by the paper: E_DEGENERATE. */
+#define RELCP_SHAPE_ELLIPSOID 0
+#define RELCP_SHAPE_SPHEROCYLINDER 1
 typedef struct relcp_bodies {
     int64_t n;
     double *pos;
@@ -115,6 +123,7 @@ typedef struct relcp_bodies {
     const double *inv_mass;
     const double *inv_inertia;
     const int32_t *kinematic;
+    const int32_t *shape;
 } relcp_bodies;
 
 /* Constraint store: SoA, append-only within a step (App. D1).

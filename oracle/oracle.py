@@ -52,6 +52,8 @@ def lib():
         i64 = ctypes.c_int64
         L.orc_snsd_batch.restype = i64
         L.orc_snsd_batch.argtypes = [i64, P, P, P, P, P, P, ctypes.c_int, P, P, P, P, P]
+        L.orc_snsd_batch_shapes.restype = i64
+        L.orc_snsd_batch_shapes.argtypes = [i64, P, P, P, P, P, P, P, ctypes.c_int, P, P, P, P, P]
         L.orc_broadphase_bruteforce.restype = i64
         L.orc_broadphase_bruteforce.argtypes = [i64, P, P, P, ctypes.c_double, P, P, i64]
         L.orc_broadphase_cells.restype = i64
@@ -95,14 +97,16 @@ def quat_to_rot(q: np.ndarray) -> np.ndarray:
     return R
 
 
-def snsd(pos, quat, axes, box, pi, pj, n_fib: int = 512):
+def snsd(pos, quat, axes, box, pi, pj, n_fib: int = 512, shape=None):
     """Shared-normal signed distance for each pair (pi[k], pj[k]) (SURVEY O1,
     P:L225 "points that minimize their shared-normal signed separation
-    distance"; P:L678-680 y_b - y_a = Phi n).
+    distance"; P:L678-680 y_b - y_a = Phi n).  shape (N,) int32: 0 ellipsoid
+    (axes = semi-axes), 1 spherocylinder (axes[0] = half-length, axes[1] =
+    radius; segment distance minus radii); None = all ellipsoids.
 
     Returns phi (P,), n (P,3) outward normal of a, ra = y_a - x_a (P,3),
-    rb = y_b - x_b (P,3), status (P,) 0 = ok, 1 = coincident centres,
-    2 = Newton not certified."""
+    rb = y_b - x_b (P,3), status (P,) 0 = ok, 1 = coincident centres /
+    intersecting centrelines, 2 = Newton not certified or mixed shapes."""
     pos, quat, axes = _c(pos, np.float64), _c(quat, np.float64), _c(axes, np.float64)
     box = _c(box if box is not None else np.zeros(3), np.float64)
     pi, pj = _c(pi, np.int32), _c(pj, np.int32)
@@ -112,9 +116,25 @@ def snsd(pos, quat, axes, box, pi, pj, n_fib: int = 512):
     ra = np.empty((P, 3))
     rb = np.empty((P, 3))
     st = np.empty(P, dtype=np.int32)
-    lib().orc_snsd_batch(P, _p(pi), _p(pj), _p(pos), _p(quat), _p(axes), _p(box), n_fib,
-                         _p(phi), _p(n), _p(ra), _p(rb), _p(st))
+    if shape is None:
+        lib().orc_snsd_batch(P, _p(pi), _p(pj), _p(pos), _p(quat), _p(axes), _p(box), n_fib,
+                             _p(phi), _p(n), _p(ra), _p(rb), _p(st))
+    else:
+        shape = _c(shape, np.int32)
+        lib().orc_snsd_batch_shapes(P, _p(pi), _p(pj), _p(pos), _p(quat), _p(axes), _p(shape), _p(box), n_fib,
+                                    _p(phi), _p(n), _p(ra), _p(rb), _p(st))
     return phi, n, ra, rb, st
+
+
+def bounding_radius(axes, shape=None):
+    """Largest distance from the centre to the surface: max semi-axis for an
+    ellipsoid, half-length + radius for a spherocylinder."""
+    axes = np.asarray(axes, dtype=np.float64)
+    r = axes.max(axis=1)
+    if shape is not None:
+        rod = np.asarray(shape) == 1
+        r = np.where(rod, axes[:, 0] + axes[:, 1], r)
+    return r
 
 
 def broadphase(pos, rad, box, margin, method: str = "auto"):
@@ -154,7 +174,7 @@ def body_W(sc, quat=None) -> np.ndarray:
         W[:, 0, 0] = W[:, 1, 1] = W[:, 2, 2] = sc["inv_mass"]
         W[:, 3:, 3:] = Iinv
     else:
-        L = 2.0 * sc["axes"].max(axis=1)
+        L = 2.0 * bounding_radius(sc["axes"], sc.get("shape"))  # 2 r_3, or l + b for rods (R22)
         xi = sc.get("xi", 1.0)
         for k in range(3):
             W[:, k, k] = 1.0 / (xi * L)
@@ -294,7 +314,8 @@ def relcp_step(sc, max_recursions: int = 50, lcp_tol: float = 1e-10, f_ext=None,
     cutoff, eps = sc["cutoff"], sc["eps_ncp"]
     box = sc["box"]
     axes = sc["axes"]
-    rad = axes.max(axis=1)
+    shape = sc.get("shape")
+    rad = bounding_radius(axes, shape)
     pos_k = sc["pos"].copy()
     quat_k = sc["quat"].copy()
     W = body_W(sc)                           # M_k^{-1} or mobility M^k, frozen at C^k
@@ -304,7 +325,7 @@ def relcp_step(sc, max_recursions: int = 50, lcp_tol: float = 1e-10, f_ext=None,
     # --- Algorithm 1 line 1: constraints A_0 between near-contacting pairs at C^k
     margin = cutoff
     pi, pj = broadphase(pos_k, rad, box, margin)
-    phi0, n0, ra0, rb0, st0 = snsd(pos_k, quat_k, axes, box, pi, pj, n_fib)
+    phi0, n0, ra0, rb0, st0 = snsd(pos_k, quat_k, axes, box, pi, pj, n_fib, shape)
     if np.any(st0 == 1):
         raise ValueError("coincident body centres (degenerate SNSD)")
     keep = phi0 < cutoff                     # reading R5
@@ -357,7 +378,7 @@ def relcp_step(sc, max_recursions: int = 50, lcp_tol: float = 1e-10, f_ext=None,
             margin = new_margin
             cand = broadphase(pos_k, rad, box, margin)
         ci, cj = cand
-        phin, nn, ran, rbn, stn = snsd(pos_n, quat_n, axes, box, ci, cj, n_fib)
+        phin, nn, ran, rbn, stn = snsd(pos_n, quat_n, axes, box, ci, cj, n_fib, shape)
         viol = phin < -eps                   # stopping rule, reading R10
         if not np.any(viol):
             break
@@ -405,7 +426,7 @@ def relcp_step(sc, max_recursions: int = 50, lcp_tol: float = 1e-10, f_ext=None,
         pos_out = pos_out - box * np.floor(pos_out / box)
     max_overlap = 0.0
     ci, cj = cand
-    phin, *_ = snsd(pos_n, quat_n, axes, box, ci, cj, n_fib)
+    phin, *_ = snsd(pos_n, quat_n, axes, box, ci, cj, n_fib, shape)
     if len(phin):
         max_overlap = float(max(0.0, -np.min(phin)))
     return dict(

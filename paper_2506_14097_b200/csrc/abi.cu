@@ -34,9 +34,13 @@ static int check_params(const relcp_params *p) {
 }
 
 // ------------------------------------------------------------ body kernels
-__global__ void k_radius(int64_t nb, const double *__restrict__ axes, double *__restrict__ rad) {
+// bounding radius: largest semi-axis (ellipsoid) or half-length + radius (rod)
+__global__ void k_radius(int64_t nb, const double *__restrict__ axes, const int32_t *__restrict__ shape,
+                         double *__restrict__ rad) {
     for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
-        rad[b] = fmax(axes[3 * b], fmax(axes[3 * b + 1], axes[3 * b + 2]));
+        rad[b] = (shape && shape[b] == RELCP_SHAPE_SPHEROCYLINDER)
+                     ? axes[3 * b] + axes[3 * b + 1]
+                     : fmax(axes[3 * b], fmax(axes[3 * b + 1], axes[3 * b + 2]));
 }
 
 // U_free = U^k + dt M^-1 F_ext (inertial, kinematic: U^k) or
@@ -228,8 +232,8 @@ static int grow_pair_tmp(relcp_ctx *ctx, int64_t np) {
 
 // SNSD over the context's pairs at (pos, Sig); flag Phi < thresh; scan.
 // Returns the number of flagged pairs in *nflag, min phi, counts.
-static int snsd_flag_scan(relcp_ctx *ctx, const double *pos, double thresh, int *nflag, double *minphi,
-                          int64_t *ndegen, int64_t *nnonconv) {
+static int snsd_flag_scan(relcp_ctx *ctx, const double *pos, const int32_t *shape, double thresh, int *nflag,
+                          double *minphi, int64_t *ndegen, int64_t *nnonconv) {
     const int64_t np = ctx->npairs;
     CKS(grow_pair_tmp(ctx, np));
     *nflag = 0;
@@ -241,7 +245,7 @@ static int snsd_flag_scan(relcp_ctx *ctx, const double *pos, double thresh, int 
     // pairs whose lower bound Phi >= F(d/|d|) is >= max(thresh, 0) can neither be
     // flagged nor lower min(Phi) below 0: they are not solved (status 3)
     CKS(geo_snsd(ctx, np, ctx->pi.p, ctx->pj.p, pos, ctx->Sig.p, ctx->tphi.p, ctx->tn.p, ctx->tra.p, ctx->trb.p,
-                 ctx->tstat.p, np, thresh > 0.0 ? thresh : 0.0));
+                 ctx->tstat.p, np, thresh > 0.0 ? thresh : 0.0, shape));
     k_flag<<<grid_for(np), RELCP_NT, 0, ctx->stream>>>(np, ctx->tphi.p, ctx->tstat.p, thresh, ctx->tflag.p,
                                                        ctx->partials.p, ctx->counter.p, ctx->red.p);
     CKL();
@@ -279,15 +283,15 @@ static double op_sigma(const relcp_ctx *ctx) { return ctx->p.dynamics == RELCP_I
 static int generate_impl(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, int64_t *n_out) {
     const int64_t nb = b->n;
     CKS(ensure_common(ctx, nb));
-    k_radius<<<grid_for(nb), RELCP_NT, 0, ctx->stream>>>(nb, b->axes, ctx->rad.p);
+    k_radius<<<grid_for(nb), RELCP_NT, 0, ctx->stream>>>(nb, b->axes, b->shape, ctx->rad.p);
     CKL();
-    CKS(geo_shape_matrices(ctx, nb, b->quat, b->axes, ctx->Sig.p));
+    CKS(geo_shape_matrices(ctx, nb, b->quat, b->axes, b->shape, ctx->Sig.p));
     ctx->margin = ctx->p.cutoff > 0.0 ? ctx->p.cutoff : 1e-3;
     CKS(geo_broadphase(ctx, nb, b->pos, ctx->rad.p, ctx->margin));
     int nflag;
     double minphi;
     int64_t ndeg, nnc;
-    CKS(snsd_flag_scan(ctx, b->pos, ctx->p.cutoff, &nflag, &minphi, &ndeg, &nnc));
+    CKS(snsd_flag_scan(ctx, b->pos, b->shape, ctx->p.cutoff, &nflag, &minphi, &ndeg, &nnc));
     ctx->step_nb = nb;
     ctx->step_pos_key = b->pos;
     ctx->op_nc = -1;
@@ -334,11 +338,11 @@ static int check_impl(relcp_ctx *ctx, const relcp_bodies *Ck, relcp_constraints 
         ctx->margin = m;
         CKS(geo_broadphase(ctx, nb, Ck->pos, ctx->rad.p, m));
     }
-    CKS(geo_shape_matrices(ctx, nb, ctx->qtrial.p, Ck->axes, ctx->Sig.p));
+    CKS(geo_shape_matrices(ctx, nb, ctx->qtrial.p, Ck->axes, Ck->shape, ctx->Sig.p));
     int nflag;
     double minphi;
     int64_t ndeg, nnc;
-    CKS(snsd_flag_scan(ctx, ctx->ptrial.p, -ctx->p.eps_ncp, &nflag, &minphi, &ndeg, &nnc));
+    CKS(snsd_flag_scan(ctx, ctx->ptrial.p, Ck->shape, -ctx->p.eps_ncp, &nflag, &minphi, &ndeg, &nnc));
     ctx->snsd_nonconv_total += nnc;
     if (min_phi) *min_phi = minphi;
     if (n_app) *n_app = nflag;
@@ -662,8 +666,8 @@ int relcp_snsd_pairs(relcp_ctx *ctx, const relcp_bodies *b, int64_t n_pairs, con
     if (n_pairs == 0) return RELCP_OK;
     if (!pi || !pj || !phi || !nrm || !ra || !rb || !status) return set_err(ctx, RELCP_E_ARG, "snsd: null output");
     CK(ctx->Sig.grow(6 * b->n));
-    CKS(geo_shape_matrices(ctx, b->n, b->quat, b->axes, ctx->Sig.p));
-    CKS(geo_snsd(ctx, n_pairs, pi, pj, b->pos, ctx->Sig.p, phi, nrm, ra, rb, status, n_pairs, INFINITY));
+    CKS(geo_shape_matrices(ctx, b->n, b->quat, b->axes, b->shape, ctx->Sig.p));
+    CKS(geo_snsd(ctx, n_pairs, pi, pj, b->pos, ctx->Sig.p, phi, nrm, ra, rb, status, n_pairs, INFINITY, b->shape));
     ctx->step_nb = -1;  // Sig overwritten
     return RELCP_OK;
 }

@@ -184,9 +184,11 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
 int scan_exclusive_ll(relcp_ctx *ctx, const long long *in, long long *out, int64_t n, long long *total_host);
 int scan_exclusive_int(relcp_ctx *ctx, const int *in, int *out, int64_t n, int *total_host);
 // geometry.cu
-int geo_shape_matrices(relcp_ctx *ctx, int64_t nb, const double *quat, const double *axes, double *Sig);
+int geo_shape_matrices(relcp_ctx *ctx, int64_t nb, const double *quat, const double *axes, const int32_t *shape,
+                       double *Sig);
 int geo_broadphase(relcp_ctx *ctx, int64_t nb, const double *pos, const double *rad, double margin);
 // reject_above: pairs whose rigorous lower bound Phi >= F(d/|d|) reaches it are
 // not solved (status 3, phi = the bound); +INFINITY = solve every pair.
 int geo_snsd(relcp_ctx *ctx, int64_t np, const int *pi, const int *pj, const double *pos, const double *Sig,
-             double *phi, double *nrm, double *ra, double *rb, int *status, int64_t planes, double reject_above);
+             double *phi, double *nrm, double *ra, double *rb, int *status, int64_t planes, double reject_above,
+             const int32_t *shape);

@@ -20,9 +20,12 @@
 #include "reduce.cuh"
 
 // ------------------------------------------------------------ shape matrices
-// Sig (nb, 6) = (xx, xy, xz, yy, yz, zz) of R diag(e^2) R^T, q normalised.
+// Per-body geometry slot Sig (nb, 6), q normalised:
+//   ellipsoid      (xx, xy, xz, yy, yz, zz) of R diag(e^2) R^T
+//   spherocylinder (u_x, u_y, u_z, h, r, 0): centreline direction u = R e_x,
+//                  half-length h = axes[0], cap radius r = axes[1]
 __global__ void k_shape(int64_t nb, const double *__restrict__ quat, const double *__restrict__ axes,
-                        double *__restrict__ Sig) {
+                        const int32_t *__restrict__ shape, double *__restrict__ Sig) {
     for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
         double s = quat[4 * b], x = quat[4 * b + 1], y = quat[4 * b + 2], z = quat[4 * b + 3];
         double inv = 1.0 / sqrt(s * s + x * x + y * y + z * z);
@@ -30,19 +33,71 @@ __global__ void k_shape(int64_t nb, const double *__restrict__ quat, const doubl
         const double R[3][3] = {{1 - 2 * (y * y + z * z), 2 * (x * y - s * z), 2 * (x * z + s * y)},
                                 {2 * (x * y + s * z), 1 - 2 * (x * x + z * z), 2 * (y * z - s * x)},
                                 {2 * (x * z - s * y), 2 * (y * z + s * x), 1 - 2 * (x * x + y * y)}};
+        double *o = Sig + 6 * b;
+        if (shape && shape[b] == RELCP_SHAPE_SPHEROCYLINDER) {
+            o[0] = R[0][0]; o[1] = R[1][0]; o[2] = R[2][0];
+            o[3] = axes[3 * b]; o[4] = axes[3 * b + 1]; o[5] = 0.0;
+            continue;
+        }
         const double e0 = axes[3 * b] * axes[3 * b], e1 = axes[3 * b + 1] * axes[3 * b + 1],
                      e2 = axes[3 * b + 2] * axes[3 * b + 2];
         auto S = [&](int i, int j) { return R[i][0] * e0 * R[j][0] + R[i][1] * e1 * R[j][1] + R[i][2] * e2 * R[j][2]; };
-        double *o = Sig + 6 * b;
         o[0] = S(0, 0); o[1] = S(0, 1); o[2] = S(0, 2);
         o[3] = S(1, 1); o[4] = S(1, 2); o[5] = S(2, 2);
     }
 }
 
-int geo_shape_matrices(relcp_ctx *ctx, int64_t nb, const double *quat, const double *axes, double *Sig) {
-    k_shape<<<grid_for(nb), RELCP_NT, 0, ctx->stream>>>(nb, quat, axes, Sig);
+int geo_shape_matrices(relcp_ctx *ctx, int64_t nb, const double *quat, const double *axes, const int32_t *shape,
+                       double *Sig) {
+    k_shape<<<grid_for(nb), RELCP_NT, 0, ctx->stream>>>(nb, quat, axes, shape, Sig);
     CKL();
     return RELCP_OK;
+}
+
+// Spherocylinder pair: closest points of the two centreline segments
+// (clamp-and-recompute solution of the convex quadratic
+// |d + t u_b - s u_a|^2 on [-h_a, h_a] x [-h_b, h_b]), minus the cap radii.
+// Parallel axes: midpoint of the overlap of the projections on u_a (R22).
+__device__ int rod_pair(const double *d, const double *ga, const double *gb, double &phi, double *nout, double *ra,
+                        double *rb) {
+    const double ua[3] = {ga[0], ga[1], ga[2]}, ub[3] = {gb[0], gb[1], gb[2]};
+    const double ha = ga[3], rra = ga[4], hb = gb[3], rrb = gb[4];
+    const double c = ua[0] * ub[0] + ua[1] * ub[1] + ua[2] * ub[2];
+    const double da = ua[0] * d[0] + ua[1] * d[1] + ua[2] * d[2];
+    const double db = ub[0] * d[0] + ub[1] * d[1] + ub[2] * d[2];
+    const double cx = ua[1] * ub[2] - ua[2] * ub[1], cy = ua[2] * ub[0] - ua[0] * ub[2],
+                 cz = ua[0] * ub[1] - ua[1] * ub[0];
+    const double cr2 = cx * cx + cy * cy + cz * cz;
+    double s, t;
+    if (sqrt(cr2) < 1e-12) {
+        const double sg = c > 0.0 ? 1.0 : -1.0;
+        const double lo = fmax(-ha, da - hb), hi = fmin(ha, da + hb);
+        s = lo <= hi ? 0.5 * (lo + hi) : (da > 0.0 ? ha : -ha);
+        t = sg * (fmin(fmax(s, da - hb), da + hb) - da);
+    } else {
+        s = fmin(fmax((da - c * db) / cr2, -ha), ha);
+        t = c * s - db;
+        if (t < -hb || t > hb) {
+            t = fmin(fmax(t, -hb), hb);
+            s = fmin(fmax(da + c * t, -ha), ha);
+        }
+    }
+    double v[3];
+    for (int k = 0; k < 3; ++k) v[k] = d[k] + t * ub[k] - s * ua[k];
+    const double dist = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    if (!(dist >= 1e-12)) {
+        phi = nan("");
+        for (int k = 0; k < 3; ++k) nout[k] = ra[k] = rb[k] = nan("");
+        return 1;  // intersecting centrelines: no normal
+    }
+    phi = dist - rra - rrb;
+    for (int k = 0; k < 3; ++k) {
+        const double nk = v[k] / dist;
+        nout[k] = nk;
+        ra[k] = s * ua[k] + rra * nk;
+        rb[k] = t * ub[k] - rrb * nk;
+    }
+    return 0;
 }
 
 // ------------------------------------------------------------ SNSD device code
@@ -310,13 +365,25 @@ __global__ void __launch_bounds__(128) k_snsd_stage1(int64_t np, const int *__re
                                                      double *__restrict__ phi, double *__restrict__ nrm,
                                                      double *__restrict__ ra, double *__restrict__ rb,
                                                      int *__restrict__ status, int64_t planes, int *multi,
-                                                     unsigned *n_multi) {
+                                                     unsigned *n_multi, const int32_t *__restrict__ shape) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < np; k += (int64_t)gridDim.x * blockDim.x) {
         double d[3];
         Sym Sa, Sb;
         pair_geom(k, pi, pj, pos, Sig, box, d, Sa, Sb);
         double f, n[3], r1[3], r2[3];
-        int st = snsd_stage1(d, Sa, Sb, reject_above, f, n, r1, r2);
+        int st;
+        const int sha = shape ? shape[pi[k]] : 0, shb = shape ? shape[pj[k]] : 0;
+        if (sha == RELCP_SHAPE_SPHEROCYLINDER && shb == RELCP_SHAPE_SPHEROCYLINDER) {
+            const double ga[6] = {Sa.xx, Sa.xy, Sa.xz, Sa.yy, Sa.yz, Sa.zz};
+            const double gb[6] = {Sb.xx, Sb.xy, Sb.xz, Sb.yy, Sb.yz, Sb.zz};
+            st = rod_pair(d, ga, gb, f, n, r1, r2);
+        } else if (sha != shb) {  // mixed ellipsoid-rod pairs are not defined (include/relcp.h)
+            f = nan("");
+            for (int c = 0; c < 3; ++c) n[c] = r1[c] = r2[c] = nan("");
+            st = SNSD_DEGENERATE;
+        } else {
+            st = snsd_stage1(d, Sa, Sb, reject_above, f, n, r1, r2);
+        }
         store_pair(k, planes, f, n, r1, r2, phi, nrm, ra, rb);
         if (st == SNSD_MULTI || st == -SNSD_MULTI) {
             multi[atomicAdd(n_multi, 1u)] = (int)k;
@@ -350,7 +417,8 @@ __global__ void __launch_bounds__(128) k_snsd_stage2(const int *__restrict__ mul
 }
 
 int geo_snsd(relcp_ctx *ctx, int64_t np, const int *pi, const int *pj, const double *pos, const double *Sig,
-             double *phi, double *nrm, double *ra, double *rb, int *status, int64_t planes, double reject_above) {
+             double *phi, double *nrm, double *ra, double *rb, int *status, int64_t planes, double reject_above,
+             const int32_t *shape) {
     if (np <= 0) return RELCP_OK;
     Box3 bx;
     for (int k = 0; k < 3; ++k) bx.v[k] = ctx->p.box[k];
@@ -361,7 +429,7 @@ int geo_snsd(relcp_ctx *ctx, int64_t np, const int *pi, const int *pj, const dou
     int64_t g = (np + 127) / 128;
     if (g > 148 * 64) g = 148 * 64;
     k_snsd_stage1<<<(unsigned)g, 128, 0, ctx->stream>>>(np, pi, pj, pos, Sig, bx, reject_above, phi, nrm, ra, rb,
-                                                        status, planes, ctx->multi.p, ctx->counter.p + 1);
+                                                        status, planes, ctx->multi.p, ctx->counter.p + 1, shape);
     CKL();
     k_snsd_stage2<<<148 * 8, 128, 0, ctx->stream>>>(ctx->multi.p, ctx->counter.p + 1, pi, pj, pos, Sig, bx, nd, phi,
                                                     nrm, ra, rb, status, planes);

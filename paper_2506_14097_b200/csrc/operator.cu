@@ -39,7 +39,7 @@
 __global__ void k_build_W(int64_t nb, int dyn, double xi, const double *__restrict__ quat,
                           const double *__restrict__ axes, const double *__restrict__ inv_mass,
                           const double *__restrict__ inv_inertia, const int32_t *__restrict__ kin,
-                          double *__restrict__ W) {
+                          const int32_t *__restrict__ shape, double *__restrict__ W) {
     for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
         double w[7];
         if (dyn == RELCP_INERTIAL) {
@@ -55,7 +55,10 @@ __global__ void k_build_W(int64_t nb, int dyn, double xi, const double *__restri
             w[1] = S(0, 0); w[2] = S(0, 1); w[3] = S(0, 2);
             w[4] = S(1, 1); w[5] = S(1, 2); w[6] = S(2, 2);
         } else {
-            double L = 2.0 * fmax(axes[3 * b], fmax(axes[3 * b + 1], axes[3 * b + 2]));
+            // drag length: 2 r_3 (ellipsoid), l + b (rod, R22)
+            double L = (shape && shape[b] == RELCP_SHAPE_SPHEROCYLINDER)
+                           ? 2.0 * (axes[3 * b] + axes[3 * b + 1])
+                           : 2.0 * fmax(axes[3 * b], fmax(axes[3 * b + 1], axes[3 * b + 2]));
             double r = 12.0 / (xi * L * L * L);
             w[0] = 1.0 / (xi * L);
             w[1] = r; w[2] = 0.0; w[3] = 0.0; w[4] = r; w[5] = 0.0; w[6] = r;
@@ -72,7 +75,7 @@ int op_build_W(relcp_ctx *ctx, const relcp_bodies *b, double *W) {
     if (ctx->p.dynamics == RELCP_OVERDAMPED && !b->axes)
         return set_err(ctx, RELCP_E_ARG, "overdamped dynamics needs axes");
     k_build_W<<<grid_for(b->n), RELCP_NT, 0, ctx->stream>>>(b->n, ctx->p.dynamics, ctx->p.xi, b->quat, b->axes,
-                                                            b->inv_mass, b->inv_inertia, b->kinematic, W);
+                                                            b->inv_mass, b->inv_inertia, b->kinematic, b->shape, W);
     CKL();
     return RELCP_OK;
 }

@@ -60,10 +60,15 @@ def growth(sc, steps: int = 10, rate: float = 0.01, capacity_per_body: int = 16,
     bodies = R.BodyState.from_scene(sc)
     cs = R.ConstraintStore(capacity_per_body * sc["n"] + 1024)
     grow = torch.as_tensor(sc["growing"], device=bodies.axes.device)
+    shape = sc.get("shape")
+    rods = shape is not None and bool((shape == 1).all())  # colony rods: l_dot = l
     reps = []
     for k in range(steps):
         if k > 0:
-            bodies.axes[grow, 0] += rate
+            if rods:
+                bodies.axes[grow, 0] *= math.exp(sc["dt"])
+            else:
+                bodies.axes[grow, 0] += rate
         rep = ctx.step(bodies, cs)
         rep.update(step=k)
         reps.append(rep)

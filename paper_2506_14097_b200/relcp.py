@@ -43,7 +43,7 @@ SOLVER_BB, SOLVER_APGD, SOLVER_APGD_FUSED = 0, 1, 2
 
 class Bodies(ctypes.Structure):
     _fields_ = [("n", i64), ("pos", P), ("quat", P), ("axes", P), ("vel", P), ("inv_mass", P),
-                ("inv_inertia", P), ("kinematic", P)]
+                ("inv_inertia", P), ("kinematic", P), ("shape", P)]
 
 
 class Constraints(ctypes.Structure):
@@ -151,7 +151,7 @@ class BodyState:
     """Device-resident SoA body arrays (fp64; kinematic int32)."""
 
     def __init__(self, pos, quat, axes, vel=None, inv_mass=None, inv_inertia=None, kinematic=None,
-                 device="cuda"):
+                 device="cuda", shape=None):
         def t(a, dt=torch.float64):
             if a is None:
                 return None
@@ -160,16 +160,17 @@ class BodyState:
         self.pos, self.quat, self.axes = t(pos), t(quat), t(axes)
         self.vel, self.inv_mass, self.inv_inertia = t(vel), t(inv_mass), t(inv_inertia)
         self.kinematic = t(kinematic, torch.int32)
+        self.shape = t(shape, torch.int32)
         self.n = self.pos.shape[0]
 
     @classmethod
     def from_scene(cls, sc, device="cuda"):
         return cls(sc["pos"], sc["quat"], sc["axes"], sc.get("vel"), sc.get("inv_mass"), sc.get("inv_inertia"),
-                   sc.get("kinematic"), device=device)
+                   sc.get("kinematic"), device=device, shape=sc.get("shape"))
 
     def view(self) -> Bodies:
         return Bodies(self.n, _ptr(self.pos), _ptr(self.quat), _ptr(self.axes), _ptr(self.vel), _ptr(self.inv_mass),
-                      _ptr(self.inv_inertia), _ptr(self.kinematic))
+                      _ptr(self.inv_inertia), _ptr(self.kinematic), _ptr(self.shape))
 
 
 class ConstraintStore:
