@@ -313,6 +313,48 @@ def cfg4(seed: int = 4, n_side: int = 1000, R: float = 1.0, r: float = 0.2, pitc
                 eps_ncp=1e-5, lcp_tol=1e-8, seed=seed, network=net)
 
 
+def chain_tori(n: int = 200, seed: int = 8, R: float = 1.0, r: float = 0.2, pitch: float = 1.58,
+               jitter: float = 0.02, dt: float = 1e-2, pull: float = 3.0) -> dict:
+    """Linked chain of tori (the paper's chainmail rings, as a
+    1-D chain): ring k at x = k * pitch with ring axis z (even k) or y (odd
+    k), so every ring passes through its neighbours' disks.  At pitch 1.58 the
+    centreline circles of neighbours are 0.42 apart (Phi = 0.42 - 2 r = 0.02:
+    near contact).  Seeded jitter (positions U(+-jitter), small rotations),
+    end rings kinematic with velocity -pull / +pull along x, interior velocity
+    the affine pull field plus N(0, 1) (u and omega), torus inertia (SURVEY
+    G9), inertial, dt = 1e-2."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    pos = np.zeros((n, 3))
+    pos[:, 0] = np.arange(n) * pitch
+    pos += rng.uniform(-jitter, jitter, size=(n, 3))
+    s2 = math.sqrt(0.5)
+    quat = np.zeros((n, 4))
+    quat[0::2] = [1.0, 0.0, 0.0, 0.0]
+    quat[1::2] = [s2, -s2, 0.0, 0.0]  # body z -> world y
+    tilt = rng.normal(scale=jitter, size=(n, 3))  # small rotation vectors
+    ang = np.linalg.norm(tilt, axis=1, keepdims=True)
+    dq = np.concatenate([np.cos(ang / 2), np.sin(ang / 2) * tilt / np.maximum(ang, 1e-300)], axis=1)
+    # quaternion product dq (x) quat
+    w1, v1 = dq[:, :1], dq[:, 1:]
+    w2, v2 = quat[:, :1], quat[:, 1:]
+    quat = np.concatenate([w1 * w2 - (v1 * v2).sum(1, keepdims=True), w1 * v2 + w2 * v1 + np.cross(v1, v2)], axis=1)
+    quat /= np.linalg.norm(quat, axis=1, keepdims=True)
+    m = 2.0 * math.pi ** 2 * R * r * r
+    I_axis = m * (R * R + 0.75 * r * r)
+    I_diam = m * (0.5 * R * R + 0.625 * r * r)
+    kin = np.zeros(n, dtype=np.int32)
+    kin[0] = kin[-1] = 1
+    vel = rng.standard_normal((n, 6))
+    vel[:, 0] += pull * (-1.0 + 2.0 * np.arange(n) / (n - 1))
+    vel[0] = [-pull, 0, 0, 0, 0, 0]
+    vel[-1] = [pull, 0, 0, 0, 0, 0]
+    return dict(name=f"chain{n}", n=n, pos=pos, quat=quat, axes=np.tile([R, r, r], (n, 1)),
+                shape=np.full(n, 2, dtype=np.int32), vel=vel, inv_mass=np.full(n, 1.0 / m),
+                inv_inertia=np.tile([1.0 / I_diam, 1.0 / I_diam, 1.0 / I_axis], (n, 1)), kinematic=kin,
+                box=np.zeros(3), dt=float(dt), dynamics=INERTIAL, xi=1.0, cutoff=0.1, eps_ncp=1e-5,
+                lcp_tol=1e-8, seed=seed)
+
+
 def random_constraint_network(n_bodies: int, n_con: int, seed: int,
                               dynamics: int = INERTIAL):
     """Random Jacobian data for operator-level tests: body pairs (a<b),

@@ -110,10 +110,15 @@ typedef struct relcp_params {
  *               RELCP_SHAPE_SPHEROCYLINDER (axes[0] = half the centreline
  *               length l/2 along body x, axes[1] = cap radius r; SNSD =
  *               segment distance minus radii; drag length l + 2r);
- *               NULL = all ellipsoids.  Mixed ellipsoid-rod pairs are not
- *               defined by the paper: E_DEGENERATE. */
+ *               or RELCP_SHAPE_TORUS (axes[0] = major radius R of the
+ *               centreline circle in the body x-y plane, axes[1] = minor radius
+ *               r; SNSD = centreline-circle distance minus radii, P:L1080;
+ *               drag length 2 (R + r));
+ *               NULL = all ellipsoids.  Mixed-shape pairs are not defined by
+ *               the paper: E_DEGENERATE. */
 #define RELCP_SHAPE_ELLIPSOID 0
 #define RELCP_SHAPE_SPHEROCYLINDER 1
+#define RELCP_SHAPE_TORUS 2
 typedef struct relcp_bodies {
     int64_t n;
     double *pos;

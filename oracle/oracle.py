@@ -128,12 +128,12 @@ def snsd(pos, quat, axes, box, pi, pj, n_fib: int = 512, shape=None):
 
 def bounding_radius(axes, shape=None):
     """Largest distance from the centre to the surface: max semi-axis for an
-    ellipsoid, half-length + radius for a spherocylinder."""
+    ellipsoid, half-length + radius for a spherocylinder, R + r for a torus."""
     axes = np.asarray(axes, dtype=np.float64)
     r = axes.max(axis=1)
     if shape is not None:
-        rod = np.asarray(shape) == 1
-        r = np.where(rod, axes[:, 0] + axes[:, 1], r)
+        sum_shape = np.isin(np.asarray(shape), (1, 2))
+        r = np.where(sum_shape, axes[:, 0] + axes[:, 1], r)
     return r
 
 

@@ -339,9 +339,126 @@ int orc_rod_pair(const double xa[3], const double qa[4], double ha, double rra, 
     return ORC_OK;
 }
 
+/* ------------------------------------------------------------------ tori */
+
+/* Torus = tube of radius r around the centreline circle of radius R in the
+ * body x-y plane (ring axis = body z).  SNSD of two tori (P:L1080 / S:L56:
+ * "two-dimensional minimization" of the centreline distance minus the minor
+ * radii): Phi = min_{theta_a, theta_b} |c_b(theta_b) - c_a(theta_a)| - r_a - r_b.
+ * The inner minimum over theta_b has a closed form (nearest point of circle b
+ * to a point: project into b's plane and scale to R_b), so the oracle samples
+ * theta_a densely (4096), refines EVERY sampled local minimum by golden
+ * section (200 iterations) and keeps the global one.  Set-valued minima
+ * ("deterministic selection rule", DESIGN R23): values within
+ * 1e-13 max(1, D) count as ties; the smallest theta_a in [0, 2 pi) wins.
+ * A point on b's axis has no unique nearest point: b's body x direction. */
+typedef struct {
+    double c[3], e1[3], e2[3], ax[3], R;
+} ring_t;
+
+static void ring_of(const double x[3], const double q[4], double R, ring_t *g) {
+    double M[9];
+    quat_to_rot(q, M);
+    for (int k = 0; k < 3; ++k) {
+        g->c[k] = x[k];
+        g->e1[k] = M[3 * k];
+        g->e2[k] = M[3 * k + 1];
+        g->ax[k] = M[3 * k + 2];
+    }
+    g->R = R;
+}
+
+static void ring_point(const ring_t *g, double th, double p[3]) {
+    const double cs = cos(th), sn = sin(th);
+    for (int k = 0; k < 3; ++k) p[k] = g->c[k] + g->R * (cs * g->e1[k] + sn * g->e2[k]);
+}
+
+/* nearest point of ring b to p; returns the squared distance */
+static double ring_nearest(const ring_t *b, const double p[3], double out[3]) {
+    double q[3], qp[3];
+    for (int k = 0; k < 3; ++k) q[k] = p[k] - b->c[k];
+    const double h = dot3(q, b->ax);
+    for (int k = 0; k < 3; ++k) qp[k] = q[k] - h * b->ax[k];
+    const double l = sqrt(dot3(qp, qp));
+    for (int k = 0; k < 3; ++k)
+        out[k] = b->c[k] + (l > 1e-14 * (1.0 + b->R) ? b->R * qp[k] / l : b->R * b->e1[k]);
+    double v[3] = {out[0] - p[0], out[1] - p[1], out[2] - p[2]};
+    return dot3(v, v);
+}
+
+static double ring_fa(const ring_t *a, const ring_t *b, double th) {
+    double p[3], o[3];
+    ring_point(a, th, p);
+    return ring_nearest(b, p, o);
+}
+
+/* d/dtheta of ring_fa (envelope theorem: the inner nearest point is stationary):
+ * 2 (p - q) . p'(theta), p'(theta) = R (-sin e1 + cos e2) */
+static double ring_dfa(const ring_t *a, const ring_t *b, double th) {
+    double p[3], q[3];
+    ring_point(a, th, p);
+    ring_nearest(b, p, q);
+    const double cs = cos(th), sn = sin(th);
+    double acc = 0.0;
+    for (int k = 0; k < 3; ++k) acc += (p[k] - q[k]) * a->R * (-sn * a->e1[k] + cs * a->e2[k]);
+    return 2.0 * acc;
+}
+
+int orc_torus_pair(const double xa[3], const double qa[4], double Ra, double rra, const double xb[3],
+                   const double qb[4], double Rb, double rrb, const double box[3], double out[10]) {
+    double d[3], xa0[3] = {0, 0, 0};
+    min_image(xa, xb, box, d);
+    ring_t A, B;
+    ring_of(xa0, qa, Ra, &A);
+    ring_of(d, qb, Rb, &B); /* frame centred on a */
+    enum { NS = 4096 };
+    static const double TWO_PI = 6.283185307179586476925;
+    double fs[NS];
+    for (int i = 0; i < NS; ++i) fs[i] = ring_fa(&A, &B, TWO_PI * i / NS);
+    double best_th = 0.0, best_f = INFINITY;
+    for (int i = 0; i < NS; ++i) {
+        const double fm = fs[(i + NS - 1) % NS], fp = fs[(i + 1) % NS];
+        if (!(fs[i] <= fm && fs[i] <= fp)) continue; /* not a sampled local minimum */
+        /* bisection on the sign change of d f / d theta inside the bracket */
+        double lo = TWO_PI * (i - 1) / NS, hi = TWO_PI * (i + 1) / NS, th = TWO_PI * i / NS;
+        /* a flat (set-valued) neighbourhood keeps the exact sample angle */
+        const int strict = fs[i] < fm && fs[i] < fp;
+        if (strict && ring_dfa(&A, &B, lo) <= 0.0 && ring_dfa(&A, &B, hi) >= 0.0) {
+            for (int it = 0; it < 100; ++it) {
+                const double mid = 0.5 * (lo + hi);
+                if (ring_dfa(&A, &B, mid) < 0.0) lo = mid; else hi = mid;
+            }
+            th = 0.5 * (lo + hi);
+        }
+        double f = ring_fa(&A, &B, th);
+        th = fmod(th, TWO_PI);
+        if (th < 0) th += TWO_PI;
+        const double tie = 1e-13 * fmax(1.0, sqrt(fmax(f, best_f == INFINITY ? f : best_f)));
+        if (sqrt(f) < sqrt(best_f) - tie || (fabs(sqrt(f) - sqrt(best_f)) <= tie && th < best_th)) {
+            best_f = f;
+            best_th = th;
+        }
+    }
+    double pa[3], pb[3];
+    ring_point(&A, best_th, pa);
+    ring_nearest(&B, pa, pb);
+    double v[3] = {pb[0] - pa[0], pb[1] - pa[1], pb[2] - pa[2]};
+    const double D = sqrt(dot3(v, v));
+    if (D < 1e-12) return ORC_DEGENERATE;
+    out[0] = D - rra - rrb;
+    for (int k = 0; k < 3; ++k) {
+        const double nk = v[k] / D;
+        out[1 + k] = nk;
+        out[4 + k] = pa[k] + rra * nk;        /* y_a - x_a */
+        out[7 + k] = pb[k] - d[k] - rrb * nk; /* y_b - x_b */
+    }
+    return ORC_OK;
+}
+
 /* Batched SNSD with per-body shapes: 0 ellipsoid (axes = semi-axes), 1
- * spherocylinder (axes[0] = half-length, axes[1] = radius).  Mixed pairs are
- * not defined by the paper: status ORC_NONCONV + NaN outputs. */
+ * spherocylinder (axes[0] = half-length, axes[1] = radius), 2 torus (axes[0] =
+ * major radius R, axes[1] = minor radius r).  Mixed pairs are not defined by
+ * the paper: status ORC_NONCONV + NaN outputs. */
 int64_t orc_snsd_batch_shapes(int64_t n_pairs, const int32_t *pi, const int32_t *pj, const double *pos,
                               const double *quat, const double *axes, const int32_t *shape, const double *box,
                               int n_fib, double *phi, double *nrm, double *ra, double *rb, int32_t *status) {
@@ -356,6 +473,9 @@ int64_t orc_snsd_batch_shapes(int64_t n_pairs, const int32_t *pi, const int32_t 
         else if (shape[a] == 1 && shape[b] == 1)
             st = orc_rod_pair(pos + 3 * a, quat + 4 * a, axes[3 * a], axes[3 * a + 1], pos + 3 * b, quat + 4 * b,
                               axes[3 * b], axes[3 * b + 1], box, out);
+        else if (shape[a] == 2 && shape[b] == 2)
+            st = orc_torus_pair(pos + 3 * a, quat + 4 * a, axes[3 * a], axes[3 * a + 1], pos + 3 * b, quat + 4 * b,
+                                axes[3 * b], axes[3 * b + 1], box, out);
         else
             st = ORC_NONCONV;
         status[k] = st;

@@ -38,7 +38,7 @@ static int check_params(const relcp_params *p) {
 __global__ void k_radius(int64_t nb, const double *__restrict__ axes, const int32_t *__restrict__ shape,
                          double *__restrict__ rad) {
     for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
-        rad[b] = (shape && shape[b] == RELCP_SHAPE_SPHEROCYLINDER)
+        rad[b] = (shape && (shape[b] == RELCP_SHAPE_SPHEROCYLINDER || shape[b] == RELCP_SHAPE_TORUS))
                      ? axes[3 * b] + axes[3 * b + 1]
                      : fmax(axes[3 * b], fmax(axes[3 * b + 1], axes[3 * b + 2]));
 }
@@ -232,8 +232,8 @@ static int grow_pair_tmp(relcp_ctx *ctx, int64_t np) {
 
 // SNSD over the context's pairs at (pos, Sig); flag Phi < thresh; scan.
 // Returns the number of flagged pairs in *nflag, min phi, counts.
-static int snsd_flag_scan(relcp_ctx *ctx, const double *pos, const int32_t *shape, double thresh, int *nflag,
-                          double *minphi, int64_t *ndegen, int64_t *nnonconv) {
+static int snsd_flag_scan(relcp_ctx *ctx, const double *pos, const int32_t *shape, const double *axes,
+                          double thresh, int *nflag, double *minphi, int64_t *ndegen, int64_t *nnonconv) {
     const int64_t np = ctx->npairs;
     CKS(grow_pair_tmp(ctx, np));
     *nflag = 0;
@@ -245,7 +245,7 @@ static int snsd_flag_scan(relcp_ctx *ctx, const double *pos, const int32_t *shap
     // pairs whose lower bound Phi >= F(d/|d|) is >= max(thresh, 0) can neither be
     // flagged nor lower min(Phi) below 0: they are not solved (status 3)
     CKS(geo_snsd(ctx, np, ctx->pi.p, ctx->pj.p, pos, ctx->Sig.p, ctx->tphi.p, ctx->tn.p, ctx->tra.p, ctx->trb.p,
-                 ctx->tstat.p, np, thresh > 0.0 ? thresh : 0.0, shape));
+                 ctx->tstat.p, np, thresh > 0.0 ? thresh : 0.0, shape, axes));
     k_flag<<<grid_for(np), RELCP_NT, 0, ctx->stream>>>(np, ctx->tphi.p, ctx->tstat.p, thresh, ctx->tflag.p,
                                                        ctx->partials.p, ctx->counter.p, ctx->red.p);
     CKL();
@@ -291,7 +291,7 @@ static int generate_impl(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraint
     int nflag;
     double minphi;
     int64_t ndeg, nnc;
-    CKS(snsd_flag_scan(ctx, b->pos, b->shape, ctx->p.cutoff, &nflag, &minphi, &ndeg, &nnc));
+    CKS(snsd_flag_scan(ctx, b->pos, b->shape, b->axes, ctx->p.cutoff, &nflag, &minphi, &ndeg, &nnc));
     ctx->step_nb = nb;
     ctx->step_pos_key = b->pos;
     ctx->op_nc = -1;
@@ -342,7 +342,7 @@ static int check_impl(relcp_ctx *ctx, const relcp_bodies *Ck, relcp_constraints 
     int nflag;
     double minphi;
     int64_t ndeg, nnc;
-    CKS(snsd_flag_scan(ctx, ctx->ptrial.p, Ck->shape, -ctx->p.eps_ncp, &nflag, &minphi, &ndeg, &nnc));
+    CKS(snsd_flag_scan(ctx, ctx->ptrial.p, Ck->shape, Ck->axes, -ctx->p.eps_ncp, &nflag, &minphi, &ndeg, &nnc));
     ctx->snsd_nonconv_total += nnc;
     if (min_phi) *min_phi = minphi;
     if (n_app) *n_app = nflag;
@@ -667,7 +667,8 @@ int relcp_snsd_pairs(relcp_ctx *ctx, const relcp_bodies *b, int64_t n_pairs, con
     if (!pi || !pj || !phi || !nrm || !ra || !rb || !status) return set_err(ctx, RELCP_E_ARG, "snsd: null output");
     CK(ctx->Sig.grow(6 * b->n));
     CKS(geo_shape_matrices(ctx, b->n, b->quat, b->axes, b->shape, ctx->Sig.p));
-    CKS(geo_snsd(ctx, n_pairs, pi, pj, b->pos, ctx->Sig.p, phi, nrm, ra, rb, status, n_pairs, INFINITY, b->shape));
+    CKS(geo_snsd(ctx, n_pairs, pi, pj, b->pos, ctx->Sig.p, phi, nrm, ra, rb, status, n_pairs, INFINITY, b->shape,
+                 b->axes));
     ctx->step_nb = -1;  // Sig overwritten
     return RELCP_OK;
 }

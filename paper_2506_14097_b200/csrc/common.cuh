@@ -191,4 +191,4 @@ int geo_broadphase(relcp_ctx *ctx, int64_t nb, const double *pos, const double *
 // not solved (status 3, phi = the bound); +INFINITY = solve every pair.
 int geo_snsd(relcp_ctx *ctx, int64_t np, const int *pi, const int *pj, const double *pos, const double *Sig,
              double *phi, double *nrm, double *ra, double *rb, int *status, int64_t planes, double reject_above,
-             const int32_t *shape);
+             const int32_t *shape, const double *axes);

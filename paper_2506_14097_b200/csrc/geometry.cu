@@ -39,6 +39,13 @@ __global__ void k_shape(int64_t nb, const double *__restrict__ quat, const doubl
             o[3] = axes[3 * b]; o[4] = axes[3 * b + 1]; o[5] = 0.0;
             continue;
         }
+        if (shape && shape[b] == RELCP_SHAPE_TORUS) {
+            // ring frame: e1 = R e_x (slots 0-2) and the ring axis e3 = R e_z
+            // (slots 3-5); e2 = e3 x e1; radii (R, r) are read from axes
+            o[0] = R[0][0]; o[1] = R[1][0]; o[2] = R[2][0];
+            o[3] = R[0][2]; o[4] = R[1][2]; o[5] = R[2][2];
+            continue;
+        }
         const double e0 = axes[3 * b] * axes[3 * b], e1 = axes[3 * b + 1] * axes[3 * b + 1],
                      e2 = axes[3 * b + 2] * axes[3 * b + 2];
         auto S = [&](int i, int j) { return R[i][0] * e0 * R[j][0] + R[i][1] * e1 * R[j][1] + R[i][2] * e2 * R[j][2]; };
@@ -324,6 +331,124 @@ __device__ int snsd_stage2(const double *d, const Sym &Sa, const Sym &Sb, int n_
     return st_best;
 }
 
+// ---- tori: Phi = min over the two centreline circles of their
+// distance, minus the minor radii.  The nearest point of ring b to a point has
+// a closed form, so the search is over theta_a only: 64 samples, the two best
+// sampled local minima refined by bisection on df/dtheta (envelope theorem),
+// ties within 1e-13 max(1, D) -> smaller theta_a in [0, 2 pi) (R23).
+struct Ring {
+    double c[3], e1[3], e2[3], ax[3], R;
+};
+__device__ __forceinline__ void ring_make(const double *c, const double *g, double Rr, Ring &o) {
+    for (int k = 0; k < 3; ++k) {
+        o.c[k] = c[k];
+        o.e1[k] = g[k];
+        o.ax[k] = g[3 + k];
+    }
+    o.e2[0] = o.ax[1] * o.e1[2] - o.ax[2] * o.e1[1];
+    o.e2[1] = o.ax[2] * o.e1[0] - o.ax[0] * o.e1[2];
+    o.e2[2] = o.ax[0] * o.e1[1] - o.ax[1] * o.e1[0];
+    o.R = Rr;
+}
+__device__ __forceinline__ void ring_pt(const Ring &g, double th, double *p, double *dp) {
+    double sn, cs;
+    sincos(th, &sn, &cs);
+    for (int k = 0; k < 3; ++k) {
+        p[k] = g.c[k] + g.R * (cs * g.e1[k] + sn * g.e2[k]);
+        dp[k] = g.R * (-sn * g.e1[k] + cs * g.e2[k]);
+    }
+}
+// nearest point q of ring b to p (axis points: along e1); returns |p - q|^2
+__device__ __forceinline__ double ring_near(const Ring &b, const double *p, double *q) {
+    const double v[3] = {p[0] - b.c[0], p[1] - b.c[1], p[2] - b.c[2]};
+    const double h = v[0] * b.ax[0] + v[1] * b.ax[1] + v[2] * b.ax[2];
+    const double w[3] = {v[0] - h * b.ax[0], v[1] - h * b.ax[1], v[2] - h * b.ax[2]};
+    const double l = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+    const bool ok = l > 1e-14 * (1.0 + b.R);
+    double r2 = 0.0;
+    for (int k = 0; k < 3; ++k) {
+        q[k] = b.c[k] + (ok ? b.R * w[k] / l : b.R * b.e1[k]);
+        r2 += (q[k] - p[k]) * (q[k] - p[k]);
+    }
+    return r2;
+}
+__device__ __forceinline__ double ring_df(const Ring &a, const Ring &b, double th) {
+    double p[3], dp[3], q[3];
+    ring_pt(a, th, p, dp);
+    ring_near(b, p, q);
+    return 2.0 * ((p[0] - q[0]) * dp[0] + (p[1] - q[1]) * dp[1] + (p[2] - q[2]) * dp[2]);
+}
+
+__device__ int torus_pair(const double *d, const double *ga, const double *gb, double Ra, double rra, double Rb,
+                          double rrb, double &phi, double *nout, double *ra, double *rb) {
+    const double zero[3] = {0.0, 0.0, 0.0};
+    Ring A, B;
+    ring_make(zero, ga, Ra, A);
+    ring_make(d, gb, Rb, B);
+    constexpr int NS = 64;
+    const double two_pi = 6.283185307179586476925;
+    double f[NS];
+    for (int i = 0; i < NS; ++i) {
+        double p[3], dp[3], q[3];
+        ring_pt(A, two_pi * i / NS, p, dp);
+        f[i] = ring_near(B, p, q);
+    }
+    // the two best sampled local minima
+    int i1 = -1, i2 = -1;
+    for (int i = 0; i < NS; ++i) {
+        const double fm = f[(i + NS - 1) % NS], fp = f[(i + 1) % NS];
+        if (!(f[i] <= fm && f[i] <= fp)) continue;
+        if (i1 < 0 || f[i] < f[i1]) {
+            i2 = i1;
+            i1 = i;
+        } else if (i2 < 0 || f[i] < f[i2]) {
+            i2 = i;
+        }
+    }
+    double best_th = 0.0, best_D = INFINITY;
+    for (int c = 0; c < 2; ++c) {
+        const int i = c == 0 ? i1 : i2;
+        if (i < 0) continue;
+        double lo = two_pi * (i - 1) / NS, hi = two_pi * (i + 1) / NS, th = two_pi * i / NS;
+        const bool strict = f[i] < f[(i + NS - 1) % NS] && f[i] < f[(i + 1) % NS];  // plateau: keep the sample
+        if (strict && ring_df(A, B, lo) <= 0.0 && ring_df(A, B, hi) >= 0.0) {
+            for (int it = 0; it < 64; ++it) {
+                const double mid = 0.5 * (lo + hi);
+                if (ring_df(A, B, mid) < 0.0) lo = mid; else hi = mid;
+            }
+            th = 0.5 * (lo + hi);
+        }
+        th = fmod(th, two_pi);
+        if (th < 0.0) th += two_pi;
+        double p[3], dp[3], q[3];
+        ring_pt(A, th, p, dp);
+        const double D = sqrt(ring_near(B, p, q));
+        const double tie = 1e-13 * fmax(1.0, fmin(D, best_D));
+        if (D < best_D - tie || (fabs(D - best_D) <= tie && th < best_th)) {
+            best_D = D;
+            best_th = th;
+        }
+    }
+    double pa[3], dp[3], pb[3];
+    ring_pt(A, best_th, pa, dp);
+    ring_near(B, pa, pb);
+    const double v[3] = {pb[0] - pa[0], pb[1] - pa[1], pb[2] - pa[2]};
+    const double D = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    if (!(D >= 1e-12)) {
+        phi = nan("");
+        for (int k = 0; k < 3; ++k) nout[k] = ra[k] = rb[k] = nan("");
+        return 1;
+    }
+    phi = D - rra - rrb;
+    for (int k = 0; k < 3; ++k) {
+        const double nk = v[k] / D;
+        nout[k] = nk;
+        ra[k] = pa[k] + rra * nk;
+        rb[k] = pb[k] - d[k] - rrb * nk;
+    }
+    return 0;
+}
+
 __device__ __forceinline__ void min_image(const double *xa, const double *xb, const double *box, double *d) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -365,7 +490,8 @@ __global__ void __launch_bounds__(128) k_snsd_stage1(int64_t np, const int *__re
                                                      double *__restrict__ phi, double *__restrict__ nrm,
                                                      double *__restrict__ ra, double *__restrict__ rb,
                                                      int *__restrict__ status, int64_t planes, int *multi,
-                                                     unsigned *n_multi, const int32_t *__restrict__ shape) {
+                                                     unsigned *n_multi, const int32_t *__restrict__ shape,
+                                                     const double *__restrict__ axes) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < np; k += (int64_t)gridDim.x * blockDim.x) {
         double d[3];
         Sym Sa, Sb;
@@ -377,6 +503,11 @@ __global__ void __launch_bounds__(128) k_snsd_stage1(int64_t np, const int *__re
             const double ga[6] = {Sa.xx, Sa.xy, Sa.xz, Sa.yy, Sa.yz, Sa.zz};
             const double gb[6] = {Sb.xx, Sb.xy, Sb.xz, Sb.yy, Sb.yz, Sb.zz};
             st = rod_pair(d, ga, gb, f, n, r1, r2);
+        } else if (sha == RELCP_SHAPE_TORUS && shb == RELCP_SHAPE_TORUS) {
+            const double ga[6] = {Sa.xx, Sa.xy, Sa.xz, Sa.yy, Sa.yz, Sa.zz};
+            const double gb[6] = {Sb.xx, Sb.xy, Sb.xz, Sb.yy, Sb.yz, Sb.zz};
+            const int64_t a = pi[k], b = pj[k];
+            st = torus_pair(d, ga, gb, axes[3 * a], axes[3 * a + 1], axes[3 * b], axes[3 * b + 1], f, n, r1, r2);
         } else if (sha != shb) {  // mixed ellipsoid-rod pairs are not defined (include/relcp.h)
             f = nan("");
             for (int c = 0; c < 3; ++c) n[c] = r1[c] = r2[c] = nan("");
@@ -418,7 +549,7 @@ __global__ void __launch_bounds__(128) k_snsd_stage2(const int *__restrict__ mul
 
 int geo_snsd(relcp_ctx *ctx, int64_t np, const int *pi, const int *pj, const double *pos, const double *Sig,
              double *phi, double *nrm, double *ra, double *rb, int *status, int64_t planes, double reject_above,
-             const int32_t *shape) {
+             const int32_t *shape, const double *axes) {
     if (np <= 0) return RELCP_OK;
     Box3 bx;
     for (int k = 0; k < 3; ++k) bx.v[k] = ctx->p.box[k];
@@ -429,7 +560,8 @@ int geo_snsd(relcp_ctx *ctx, int64_t np, const int *pi, const int *pj, const dou
     int64_t g = (np + 127) / 128;
     if (g > 148 * 64) g = 148 * 64;
     k_snsd_stage1<<<(unsigned)g, 128, 0, ctx->stream>>>(np, pi, pj, pos, Sig, bx, reject_above, phi, nrm, ra, rb,
-                                                        status, planes, ctx->multi.p, ctx->counter.p + 1, shape);
+                                                        status, planes, ctx->multi.p, ctx->counter.p + 1, shape,
+                                                        axes);
     CKL();
     k_snsd_stage2<<<148 * 8, 128, 0, ctx->stream>>>(ctx->multi.p, ctx->counter.p + 1, pi, pj, pos, Sig, bx, nd, phi,
                                                     nrm, ra, rb, status, planes);

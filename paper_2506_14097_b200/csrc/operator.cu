@@ -56,7 +56,7 @@ __global__ void k_build_W(int64_t nb, int dyn, double xi, const double *__restri
             w[4] = S(1, 1); w[5] = S(1, 2); w[6] = S(2, 2);
         } else {
             // drag length: 2 r_3 (ellipsoid), l + b (rod, R22)
-            double L = (shape && shape[b] == RELCP_SHAPE_SPHEROCYLINDER)
+            double L = (shape && (shape[b] == RELCP_SHAPE_SPHEROCYLINDER || shape[b] == RELCP_SHAPE_TORUS))
                            ? 2.0 * (axes[3 * b] + axes[3 * b + 1])
                            : 2.0 * fmax(axes[3 * b], fmax(axes[3 * b + 1], axes[3 * b + 2]));
             double r = 12.0 / (xi * L * L * L);
