@@ -7,18 +7,21 @@
 //   W_b = M_b^{-1} or local-drag mobility
 //
 // B200 layout:
-//   * scatter U = W D x (K6) is a body-major CSR pass.  Each body owns a
-//     contiguous segment of signed 6-double wrench payloads, built once per
-//     operator and ordered (side, constraint): the a-side entries of a store
-//     sorted by (ia, ib) come first and reference consecutive constraints, so
-//     their x / g loads arrive in contiguous runs.  One warp owns 32 bodies
-//     (one per lane); the warp's entries are streamed in coalesced 64-entry
-//     tiles into shared memory and each lane sums its own body's entries in
-//     segment order (fixed association: bitwise deterministic, no atomics),
-//     then applies W_b (SoA planes, coalesced) and stores U_b through a
-//     shared-memory transpose (coalesced).
+//   * scatter U = W D x (K6) is a body-major pass.  One warp owns 32 bodies
+//     (one per lane).  With the library's sorted store (R18) the a-side rows
+//     of those bodies are one contiguous store range, read in place (n, t_a,
+//     x, g planes); the b-side entries come from a CSR (constraint id +
+//     signed [n; t_b] payload, built once per operator, sorted by constraint).
+//     An unsorted caller store puts both sides in the CSR.  Entries are
+//     streamed in coalesced 64-entry tiles into shared memory and each lane
+//     sums its own body's entries in order (fixed association: bitwise
+//     deterministic, no atomics), then applies W_b (SoA planes) and stores U_b
+//     through a shared-memory transpose (coalesced).  The kernel is bound by
+//     the L1 data pipe (staging + bank-conflicted per-lane sums + the b-side
+//     x / g gathers); see profiles/README.md.
 //   * gather y = s D^T U (K7) is a constraint-major streaming pass over the
 //     SoA store (coalesced n / t_a / t_b planes) with U_a, U_b read from L2.
+//   * k_fused_rows: the fused-APGD row pass (lcp.cu solver 2).
 #include "common.cuh"
 #include "reduce.cuh"
 
