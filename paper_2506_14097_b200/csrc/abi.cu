@@ -2,6 +2,8 @@
 // (Algorithm 1; inertial form Eq. relcp_inertial).
 #include <chrono>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: phase ranges for Nsight timelines
+
 #include "common.cuh"
 #include "reduce.cuh"
 
@@ -569,7 +571,9 @@ int relcp_step(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_const
                                                         b->kinematic, ctx->ufree.p);
     CKL();
     int64_t n0 = 0;
+    nvtxRangePushA("relcp_generate");
     int rc = generate_impl(ctx, b, cs, &n0);  // Alg. 1 lines 1-2
+    nvtxRangePop();
     if (rc < 0) return rc;
     int warn = rc;
     double t1 = now_ms();
@@ -578,7 +582,9 @@ int relcp_step(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_const
     for (;;) {
         relcp_solve_report sr;
         double ts = now_ms();
+        nvtxRangePushA("relcp_solve_lcp");
         rc = lcp_solve(ctx, b, cs, &sr);  // lines 3 / 10
+        nvtxRangePop();
         R.ms_solve += now_ms() - ts;
         if (rc < 0) return rc;
         if (rc == RELCP_W_MAX_ITER) warn = rc;
@@ -591,7 +597,9 @@ int relcp_step(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_const
         int64_t napp = 0;
         double minphi = INFINITY;
         const int allow = recursion < ctx->p.max_recursions;
+        nvtxRangePushA("relcp_check_and_augment");
         rc = check_impl(ctx, b, cs, recursion + 1, allow, &napp, &minphi);
+        nvtxRangePop();
         R.ms_check += now_ms() - tc;
         if (rc < 0) return rc;
         if (rc == RELCP_W_SNSD_NONCONV) warn = rc;
