@@ -74,6 +74,53 @@ def test_delassus_apply_parity(orc, R, dynamics, nb, nc):
     assert np.max(np.abs(U.cpu().numpy() - U_ref)) <= 1e-12 * np.max(np.abs(U_ref))
 
 
+@pytest.mark.parametrize("shuffled", [False, True])
+@pytest.mark.parametrize("dynamics", [0, 1])
+def test_delassus_apply_hubs_and_empty_bodies(orc, R, shuffled, dynamics):
+    """K6 tile logic: a hub body whose segment spans many 64-entry tiles (700
+    rows), a body with 130 rows to one partner, runs of bodies without rows,
+    a ragged body count; sorted (a-side in place) and unsorted (general CSR)."""
+    rng = np.random.default_rng(42)
+    nb = 1000 + 37
+    ia = [np.zeros(700, int)]
+    ib = [rng.integers(1, nb, size=700)]
+    ia.append(np.full(130, 500)); ib.append(np.full(130, 900))
+    live = rng.choice(np.arange(1, nb), size=300, replace=False)  # other bodies: sparse
+    a = rng.choice(live, size=400); b = rng.choice(live, size=400)
+    keep = a != b
+    ia.append(a[keep]); ib.append(b[keep])
+    ia, ib = np.concatenate(ia), np.concatenate(ib)
+    lo, hi = np.minimum(ia, ib), np.maximum(ia, ib)
+    o = np.lexsort((hi, lo))
+    ia, ib = lo[o].astype(np.int32), hi[o].astype(np.int32)
+    nc = len(ia)
+    n = rng.normal(size=(nc, 3))
+    n /= np.linalg.norm(n, axis=1, keepdims=True)
+    ta, tb = rng.uniform(-1, 1, size=(nc, 3)), rng.uniform(-1, 1, size=(nc, 3))
+    if shuffled:
+        p = rng.permutation(nc)
+        ia, ib, n, ta, tb = ia[p], ib[p], n[p], ta[p], tb[p]
+    b_ = scenes.suspension(nb, (1.0, 0.6, 0.4), 0.3, 5, dynamics=dynamics)
+    W = orc.body_W(b_)
+    x = rng.standard_normal(nc)
+    y_ref = orc.delassus_apply(W, ia, ib, n, ta, tb, 1.0, x)
+    F_ref, U_ref = orc.wrench(W, ia, ib, n, ta, tb, x)
+    ctx = _ctx(R, dict(dynamics=dynamics, dt=1e-3, cutoff=0.1, eps_ncp=1e-5, box=[0, 0, 0]))
+    bodies = R.BodyState.from_scene(b_)
+    cs = R.ConstraintStore.from_rows(ia, ib, n, ta, tb)
+    ctx.prepare_operator(bodies, cs)
+    xd = torch.as_tensor(x, device="cuda")
+    yd = torch.empty_like(xd)
+    ctx.delassus_apply(bodies, cs, xd, yd, 1.0)
+    assert np.max(np.abs(yd.cpu().numpy() - y_ref)) <= 1e-12 * np.max(np.abs(y_ref))
+    F = torch.empty(nb, 6, dtype=torch.float64, device="cuda")
+    U = torch.empty_like(F)
+    ctx.wrench(bodies, cs, xd, F, U)
+    assert np.max(np.abs(F.cpu().numpy() - F_ref)) <= 1e-12 * np.max(np.abs(F_ref))
+    assert np.max(np.abs(U.cpu().numpy() - U_ref)) <= 1e-12 * np.max(np.abs(U_ref))
+    assert np.all(U.cpu().numpy()[np.setdiff1d(np.arange(nb), np.concatenate([ia, ib]))] == 0)
+
+
 def test_delassus_empty_and_state(orc, R):
     b, ia, ib, n, ta, tb = _net(orc, 10, 5, 3, 0)
     ctx = _ctx(R, dict(dynamics=0, dt=1e-3, cutoff=0.1, eps_ncp=1e-5, box=[0, 0, 0]))
@@ -270,12 +317,12 @@ def _sorted_rows(ia, ib, gen):
     return np.lexsort((ib, ia, gen))
 
 
-def _compare_step(orc, R, sc, tol_cfg=1e-9, max_recursions=50):
+def _compare_step(orc, R, sc, tol_cfg=1e-9, max_recursions=50, solver=0):
     # Both sides solve every LCP to r <= 1e-12: two independent solvers that
     # each stop at r <= 1e-10 leave rotations differing by ~1e-9 (measured
     # 1.4e-9 on cfg1), at the edge of the 1e-9 configuration tolerance.
     r = orc.relcp_step(sc, lcp_tol=1e-12, max_recursions=max_recursions)
-    ctx = _ctx(R, sc, lcp_tol=1e-12, max_recursions=max_recursions, lcp_max_iter=2_000_000)
+    ctx = _ctx(R, sc, lcp_tol=1e-12, max_recursions=max_recursions, lcp_max_iter=2_000_000, solver=solver)
     bodies = R.BodyState.from_scene(sc)
     cs = R.ConstraintStore(8 * max(1, len(r["constraints"]["ia"])) + 64)
     rep = ctx.step(bodies, cs)
@@ -306,6 +353,13 @@ def _compare_step(orc, R, sc, tol_cfg=1e-9, max_recursions=50):
 
 def test_step_parity_cfg1(orc, R):
     _compare_step(orc, R, scenes.cfg1())
+
+
+@pytest.mark.parametrize("solver", [1, 2])
+def test_step_parity_cfg1_apgd(orc, R, solver):
+    """The whole step with APGD / fused APGD against the oracle's BB step
+    (solution parity: every LCP solved to r <= 1e-12 on both sides)."""
+    _compare_step(orc, R, scenes.cfg1(), solver=solver)
 
 
 def test_step_parity_overdamped_cfg2_recipe(orc, R):
