@@ -209,7 +209,11 @@ def run_ours(args, rank, world, dist):
     iters = sum(sum(r["iterations"]) for r in reports)
     assert iters == stats["lcp_iterations"], (iters, stats)
     nbytes = sum(iter_bytes(r["n_c"], r["iterations"], args.n) for r in reports)
-    it_ms = stats["scatter_ms"] + stats["gather_ms"]
+    # timed iterations: each solve's first batch (events around K6 / K7) and its
+    # complete CUDA-graph batches (events around the graph launch); the few
+    # iterations of a solve's last, partly executed batch are left out
+    it_timed = max(1, stats["iter_timed"])
+    it_ms = stats["iter_ms"] * iters / it_timed  # extrapolated to every iteration of the step
     ms_max, iters_all = combine_ranks(ms, iters, dist, dev)
     value = iters_all / (ms_max / 1e3)
 
@@ -220,7 +224,7 @@ def run_ours(args, rank, world, dist):
     peak = peaks.get("hbm_gbs")
     peak_src = "measured" if peak else "fallback"
     peak = peak or 6650.0
-    achieved = nbytes / (it_ms / 1e3) / 1e9 if it_ms > 0 else None
+    achieved = (nbytes / iters) / (stats["iter_ms"] / it_timed / 1e3) / 1e9 if stats["iter_ms"] > 0 else None
     # DRAM traffic per iteration from the committed ncu --set full capture (K6 + K7)
     traffic = traffic_ratio = traffic_nc = None
     tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -307,8 +311,10 @@ def run_ours(args, rank, world, dist):
                       unit="GB/s", frac=(achieved / peak) if achieved else None, traffic=traffic,
                       traffic_n_c=traffic_nc, traffic_over_algorithmic=traffic_ratio,
                       peak_source=peak_src, frac_of_8TBps=(achieved / 8000.0) if achieved else None,
-                      iter_ms=it_ms / max(1, stats["iter_timed"]), scatter_ms_total=stats["scatter_ms"],
-                      gather_ms_total=stats["gather_ms"], share_of_step=it_ms / ms),
+                      iter_ms=stats["iter_ms"] / it_timed, iters_timed=stats["iter_timed"],
+                      scatter_ms=stats["scatter_ms"] / max(1, stats["split_timed"]),
+                      gather_ms=stats["gather_ms"] / max(1, stats["split_timed"]),
+                      split_timed=stats["split_timed"], share_of_step=it_ms / ms),
         delassus_apply=apply,
         cpu_baseline=cpu, e2e=e2e, gpu_launches=stats["launches"], clocks=clk,
         step_report={k: last.get(k) for k in ("recursions", "status", "residuals", "max_overlap", "ms_generate",

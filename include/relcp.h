@@ -275,14 +275,23 @@ int relcp_get_pairs(relcp_ctx *ctx, int32_t *pi, int32_t *pj, int64_t cap, int64
  *   launches          kernels this context launched (all entry points)
  *   lcp_iterations    BB iterations executed (K6 scatter + K7 gather pairs)
  * and, when timing is on (relcp_set_timing(ctx, 1)), CUDA-event durations on
- * the context stream of every executed LCP iteration:
- *   scatter_ms / gather_ms  summed K6 / K7 durations, iter_timed = count. */
+ * the context stream:
+ *   iter_ms / iter_timed    summed duration / count of the timed LCP
+ *                           iterations: the first batch of each solve (direct
+ *                           launches, events around each kernel) and every
+ *                           CUDA-graph batch that ran all its iterations
+ *                           (events around the graph launch);
+ *   scatter_ms / gather_ms  summed K6 / K7 (or fused row pass / b-side scatter)
+ *                           durations over the split_timed iterations of the
+ *                           direct batches. */
 typedef struct relcp_stats {
     int64_t launches;
     int64_t lcp_iterations;
     int64_t iter_timed;
     double scatter_ms;
     double gather_ms;
+    int64_t split_timed;
+    double iter_ms;
 } relcp_stats;
 int relcp_get_stats(relcp_ctx *ctx, relcp_stats *out);
 int relcp_reset_stats(relcp_ctx *ctx);

@@ -436,7 +436,7 @@ int relcp_destroy(relcp_ctx *ctx) {
     ctx->cell_count.release(); ctx->cell_start.release(); ctx->cell_fill.release(); ctx->cell_items.release();
     ctx->body_cell.release(); ctx->pair_cnt.release(); ctx->red.release();
     if (ctx->ev_ready)
-        for (int k = 0; k < 3 * 64; ++k) cudaEventDestroy(ctx->ev[k]);
+        for (int k = 0; k < 3 * 64 + 2; ++k) cudaEventDestroy(ctx->ev[k]);
     if (ctx->st_host) cudaFreeHost(ctx->st_host);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->red_host) cudaFreeHost(ctx->red_host);
@@ -634,6 +634,8 @@ int relcp_get_stats(relcp_ctx *ctx, relcp_stats *out) {
     out->iter_timed = ctx->iter_timed;
     out->scatter_ms = ctx->scatter_ms;
     out->gather_ms = ctx->gather_ms;
+    out->split_timed = ctx->split_timed;
+    out->iter_ms = ctx->iter_ms;
     return RELCP_OK;
 }
 
@@ -641,8 +643,8 @@ int relcp_reset_stats(relcp_ctx *ctx) {
     if (!ctx) return RELCP_E_ARG;
     ctx->launches = 0;
     ctx->lcp_iterations = 0;
-    ctx->iter_timed = 0;
-    ctx->scatter_ms = ctx->gather_ms = 0.0;
+    ctx->iter_timed = ctx->split_timed = 0;
+    ctx->scatter_ms = ctx->gather_ms = ctx->iter_ms = 0.0;
     return RELCP_OK;
 }
 

@@ -121,9 +121,9 @@ struct relcp_ctx {
     int64_t launches = 0;
     int64_t lcp_iterations = 0;
     int timing = 0;
-    int64_t iter_timed = 0;
-    double scatter_ms = 0.0, gather_ms = 0.0;
-    cudaEvent_t ev[3 * 64] = {};
+    int64_t iter_timed = 0, split_timed = 0;
+    double scatter_ms = 0.0, gather_ms = 0.0, iter_ms = 0.0;
+    cudaEvent_t ev[3 * 64 + 2] = {};  // per-kernel events of a direct batch + 2 around a graph launch
     int ev_ready = 0;
 };
 

@@ -301,29 +301,31 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
     if (ctx->timing) {
         if (batch > 64) batch = 64;
         if (!ctx->ev_ready) {
-            for (int k = 0; k < 3 * 64; ++k) CK(cudaEventCreate(&ctx->ev[k]));
+            for (int k = 0; k < 3 * 64 + 2; ++k) CK(cudaEventCreate(&ctx->ev[k]));
             ctx->ev_ready = 1;
         }
     }
     long long it_before = 0;
     int pending = 0, batches = 0;
+    bool capturing = false, graph_timed = false;
     cudaGraphExec_t gexec = nullptr;
     // `batch` BB iterations: K6 (scatter + projection) then K7 (gather + update)
     auto enqueue_batch = [&]() -> int {
         for (int j = 0; j < batch; ++j) {
-            // per-iteration events only in timing mode, which never captures graphs
+            // per-kernel events only for direct (uncaptured) batches in timing mode
+            const bool ev_on = ctx->timing && !capturing;
             if (fused) {
                 // row pass (g_{k+1}, x_{k+2}, a-side sums) then the b-side scatter + W
-                if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j], st));
+                if (ev_on) CK(cudaEventRecord(ctx->ev[3 * j], st));
                 CKS(op_fused_rows(ctx, cs, nb, s, cs->lambda, xB));
-                if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j + 1], st));
+                if (ev_on) CK(cudaEventRecord(ctx->ev[3 * j + 1], st));
                 CKS(op_scatter(ctx, nb, cs->lambda, nullptr, 3, nullptr, ctx->U.p, nullptr, xB, nullptr));
-                if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j + 2], st));
+                if (ev_on) CK(cudaEventRecord(ctx->ev[3 * j + 2], st));
                 continue;
             }
-            if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j], st));
+            if (ev_on) CK(cudaEventRecord(ctx->ev[3 * j], st));
             CKS(op_scatter(ctx, nb, cs->lambda, cs->g, apgd ? 2 : 1, nullptr, ctx->U.p, nullptr, xB, gB));
-            if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j + 1], st));
+            if (ev_on) CK(cudaEventRecord(ctx->ev[3 * j + 1], st));
             if (apgd)
                 k_apgd_iter<<<gridc, RELCP_NT, 0, st>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb,
                                                         ctx->U.p, s, cs->q, cs->lambda, cs->g, xB, gB,
@@ -333,7 +335,7 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
                                                        ctx->U.p, s, cs->q, cs->lambda, cs->g, ctx->partials.p,
                                                        ctx->counter.p, ctx->st.p);
             CKL();
-            if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * j + 2], st));
+            if (ev_on) CK(cudaEventRecord(ctx->ev[3 * j + 2], st));
         }
         return RELCP_OK;
     };
@@ -342,23 +344,36 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
         CK(cudaStreamSynchronize(st));
         const long long executed = ctx->st_host->iter - it_before;
         ctx->lcp_iterations += executed;
-        if (ctx->timing && pending > 0) {
+        if (ctx->timing && pending > 0 && graph_timed) {
+            // a graph batch counts only when every one of its iterations ran
+            // (iterations after convergence exit at once and would dilute it)
+            if (executed == pending) {
+                float a = 0.f;
+                CK(cudaEventElapsedTime(&a, ctx->ev[3 * 64], ctx->ev[3 * 64 + 1]));
+                ctx->iter_ms += a;
+                ctx->iter_timed += pending;
+            }
+        } else if (ctx->timing && pending > 0) {
             for (long long j = 0; j < executed && j < pending; ++j) {
                 float a = 0.f, b2 = 0.f;
                 CK(cudaEventElapsedTime(&a, ctx->ev[3 * j], ctx->ev[3 * j + 1]));
                 CK(cudaEventElapsedTime(&b2, ctx->ev[3 * j + 1], ctx->ev[3 * j + 2]));
                 ctx->scatter_ms += a;
                 ctx->gather_ms += b2;
+                ctx->iter_ms += a + b2;
                 ++ctx->iter_timed;
+                ++ctx->split_timed;
             }
         }
         it_before = ctx->st_host->iter;
         if (ctx->st_host->done) break;
-        if (!gexec && batches >= 1 && !ctx->timing) {
+        if (!gexec && batches >= 1) {
             // the solve runs long: capture one batch as a CUDA graph, replay it
             cudaGraph_t graph = nullptr;
             CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            capturing = true;
             const int rc = enqueue_batch();
+            capturing = false;
             cudaError_t ec = cudaStreamEndCapture(st, &graph);
             ctx->launches -= 2 * batch;  // captured, not executed
             if (rc < 0) return rc;
@@ -368,7 +383,10 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
             CK(ec);
         }
         if (gexec) {
+            if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * 64], st));
             CK(cudaGraphLaunch(gexec, st));
+            if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * 64 + 1], st));
+            graph_timed = true;
             ctx->launches += 2 * batch;
         } else {
             CKS(enqueue_batch());

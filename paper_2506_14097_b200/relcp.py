@@ -58,7 +58,7 @@ class SolveReport(ctypes.Structure):
 
 class Stats(ctypes.Structure):
     _fields_ = [("launches", i64), ("lcp_iterations", i64), ("iter_timed", i64), ("scatter_ms", f64),
-                ("gather_ms", f64)]
+                ("gather_ms", f64), ("split_timed", i64), ("iter_ms", f64)]
 
 
 class StepReport(ctypes.Structure):
@@ -333,7 +333,8 @@ class Context:
         st = Stats()
         self._check(self.L.relcp_get_stats(self.h, ctypes.byref(st)))
         return dict(launches=st.launches, lcp_iterations=st.lcp_iterations, iter_timed=st.iter_timed,
-                    scatter_ms=st.scatter_ms, gather_ms=st.gather_ms)
+                    scatter_ms=st.scatter_ms, gather_ms=st.gather_ms, split_timed=st.split_timed,
+                    iter_ms=st.iter_ms)
 
     def reset_stats(self):
         self._check(self.L.relcp_reset_stats(self.h))

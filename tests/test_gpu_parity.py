@@ -394,6 +394,33 @@ def test_step_deterministic(R):
     assert all(torch.equal(a, b) for a, b in zip(out[0], out[1]))
 
 
+@pytest.mark.parametrize("solver", [0, 2])
+def test_timing_mode_same_result(R, solver):
+    """relcp_set_timing only adds CUDA events (per kernel in the first batch,
+    around each CUDA-graph replay after it): the step is bitwise the one run
+    without timing, and the stats count the timed iterations."""
+    sc = scenes.cfg1()
+    out = []
+    for timing in (False, True):
+        ctx = _ctx(R, sc, solver=solver, lcp_tol=1e-12)
+        bodies = R.BodyState.from_scene(sc)
+        cs = R.ConstraintStore(8000)
+        ctx.reset_stats()
+        ctx.set_timing(timing)
+        rep = ctx.step(bodies, cs)
+        st = ctx.stats()
+        out.append((bodies.pos.clone(), bodies.vel.clone(), cs.lam[:cs.count].clone()))
+        iters = sum(rep["iterations"])
+        assert st["lcp_iterations"] == iters
+        if timing:
+            assert iters > 64  # several batches: direct first batch + graph replays
+            assert 0 < st["split_timed"] < st["iter_timed"] <= iters
+            assert st["iter_ms"] >= st["scatter_ms"] + st["gather_ms"] - 1e-9 > 0
+        else:
+            assert st["iter_timed"] == 0 and st["iter_ms"] == 0.0
+    assert all(torch.equal(a, b) for a, b in zip(out[0], out[1]))
+
+
 # ------------------------------------------------------------ cfg3 / cfg4 recipes
 
 @pytest.mark.parametrize("solver", [0, 1, 2])

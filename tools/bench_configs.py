@@ -80,7 +80,7 @@ def run(name):
         st = ctx.stats()
         ms = a.elapsed_time(b)
         it = st["iter_timed"]
-        it_ms = (st["scatter_ms"] + st["gather_ms"]) / max(1, it)
+        it_ms = st["iter_ms"] / max(1, it)
         nc = cs.count
         out.update(n_c=nc, lcp=dict(iterations=rep["iterations"], residual=rep["residual"],
                                     converged=rep["converged"], solve_ms=ms,
@@ -113,7 +113,8 @@ def run(name):
     st = ctx.stats()
     iters = sum(rep["iterations"])
     it_bytes = sum(i * (216.0 * c + 152.0 * n) for c, i in zip(rep["n_c"], rep["iterations"]))
-    it_ms = st["scatter_ms"] + st["gather_ms"]
+    # bytes per iteration averaged over the step / time per timed iteration
+    it_ms = st["iter_ms"] / max(1, st["iter_timed"]) * iters
     out.update(step_ms=ms, recursions=rep["recursions"], status=rep["status"], n_c=rep["n_c"],
                lcp_iters=rep["iterations"], residuals=rep["residuals"], max_overlap=rep["max_overlap"],
                n_pairs=rep["n_pairs"], ms_generate=rep["ms_generate"], ms_solve=rep["ms_solve"],

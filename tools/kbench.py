@@ -51,7 +51,7 @@ ctx.set_timing(True)
 t = time.time()
 rep = ctx.solve_lcp(bodies, cs)
 st = ctx.stats()
-it = st["iter_timed"]
-print(f"solve {rep['iterations']} it in {time.time() - t:.3f}s; scatter {st['scatter_ms'] / it:.4f} ms "
-      f"gather {st['gather_ms'] / it:.4f} ms; iter alg "
-      f"{(216 * nc + 152 * n) / ((st['scatter_ms'] + st['gather_ms']) / it) / 1e6:.0f} GB/s", flush=True)
+it, sp = max(1, st["iter_timed"]), max(1, st["split_timed"])
+print(f"solve {rep['iterations']} it in {time.time() - t:.3f}s; scatter {st['scatter_ms'] / sp:.4f} ms "
+      f"gather {st['gather_ms'] / sp:.4f} ms (first batch); iter {st['iter_ms'] / it:.4f} ms over {it}; iter alg "
+      f"{(216 * nc + 152 * n) / (st['iter_ms'] / it) / 1e6:.0f} GB/s", flush=True)
