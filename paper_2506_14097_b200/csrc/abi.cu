@@ -248,6 +248,7 @@ static int snsd_flag_scan(relcp_ctx *ctx, const double *pos, const int32_t *shap
     // flagged nor lower min(Phi) below 0: they are not solved (status 3)
     CKS(geo_snsd(ctx, np, ctx->pi.p, ctx->pj.p, pos, ctx->Sig.p, ctx->tphi.p, ctx->tn.p, ctx->tra.p, ctx->trb.p,
                  ctx->tstat.p, np, thresh > 0.0 ? thresh : 0.0, shape, axes));
+    PHASE(ctx, "snsd.kernels");
     k_flag<<<grid_for(np), RELCP_NT, 0, ctx->stream>>>(np, ctx->tphi.p, ctx->tstat.p, thresh, ctx->tflag.p,
                                                        ctx->partials.p, ctx->counter.p, ctx->red.p);
     CKL();
@@ -261,6 +262,7 @@ static int snsd_flag_scan(relcp_ctx *ctx, const double *pos, const int32_t *shap
     *ndegen = (int64_t)ctx->red_host[0];
     *nnonconv = (int64_t)ctx->red_host[1];
     *minphi = ctx->red_host[2];
+    PHASE(ctx, "snsd.flag_scan");
     return RELCP_OK;
 }
 
@@ -288,8 +290,10 @@ static int generate_impl(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraint
     k_radius<<<grid_for(nb), RELCP_NT, 0, ctx->stream>>>(nb, b->axes, b->shape, ctx->rad.p);
     CKL();
     CKS(geo_shape_matrices(ctx, nb, b->quat, b->axes, b->shape, ctx->Sig.p));
+    PHASE(ctx, "gen.shape");
     ctx->margin = ctx->p.cutoff > 0.0 ? ctx->p.cutoff : 1e-3;
     CKS(geo_broadphase(ctx, nb, b->pos, ctx->rad.p, ctx->margin));
+    PHASE(ctx, "gen.broadphase");
     int nflag;
     double minphi;
     int64_t ndeg, nnc;
@@ -311,6 +315,7 @@ static int generate_impl(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraint
     CKS(op_row_dot_U(ctx, cs, 0, nflag, ctx->ufree.p, ctx->p.dt, cs->q));
     if (n_out) *n_out = nflag;
     CK(cudaStreamSynchronize(ctx->stream));
+    PHASE(ctx, "gen.append");
     return nnc > 0 ? RELCP_W_SNSD_NONCONV : RELCP_OK;
 }
 
@@ -320,7 +325,9 @@ static int check_impl(relcp_ctx *ctx, const relcp_bodies *Ck, relcp_constraints 
     const int64_t nb = Ck->n;
     if (ctx->step_nb != nb || ctx->step_pos_key != Ck->pos)
         return set_err(ctx, RELCP_E_STATE, "check_and_augment: call relcp_generate_contacts on these bodies first");
+    PHASE(ctx, "chk.enter");
     if (ctx->op_nc != cs->count || ctx->op_nb != nb || ctx->op_key_ia != cs->ia) CKS(op_prepare(ctx, Ck, cs));
+    PHASE(ctx, "chk.prepare");
     // Uc = W D lambda
     if (cs->count > 0)
         CKS(op_scatter(ctx, nb, cs->lambda, nullptr, 0, nullptr, ctx->U.p, nullptr));
@@ -333,6 +340,7 @@ static int check_impl(relcp_ctx *ctx, const relcp_bodies *Ck, relcp_constraints 
     CK(cudaMemcpyAsync(ctx->red_host, ctx->red.p, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     const double delta = ctx->red_host[0];
+    PHASE(ctx, "chk.scatter_trial");
     // R7: widen the candidate margin until it exceeds the largest approach 2 delta
     double m = ctx->margin;
     while (m <= 2.0 * delta) m *= 2.0;
@@ -340,7 +348,9 @@ static int check_impl(relcp_ctx *ctx, const relcp_bodies *Ck, relcp_constraints 
         ctx->margin = m;
         CKS(geo_broadphase(ctx, nb, Ck->pos, ctx->rad.p, m));
     }
+    PHASE(ctx, "chk.broadphase");
     CKS(geo_shape_matrices(ctx, nb, ctx->qtrial.p, Ck->axes, Ck->shape, ctx->Sig.p));
+    PHASE(ctx, "chk.shape");
     int nflag;
     double minphi;
     int64_t ndeg, nnc;
@@ -358,12 +368,15 @@ static int check_impl(relcp_ctx *ctx, const relcp_bodies *Ck, relcp_constraints 
     const int64_t base = cs->count;
     CKS(append_flagged(ctx, cs, gen, nflag));
     cs->count = base + nflag;
+    PHASE(ctx, "chk.append");
     // q_new = Phi(C_n) - s row . (W D lambda)   (b_n = A_n iota(x) - Phi~)
     CKS(op_row_dot_U(ctx, cs, base, base + nflag, ctx->U.p, -op_s(ctx), cs->q));
     // keep the store sorted by (ia, ib, gen) (R18): stable merge of the new block
+    PHASE(ctx, "chk.rowdot");
     CKS(store_merge_appended(ctx, cs, base, nflag));
     ctx->op_nc = -1;
     CK(cudaStreamSynchronize(ctx->stream));
+    PHASE(ctx, "chk.merge");
     return nnc > 0 ? RELCP_W_SNSD_NONCONV : RELCP_OK;
 }
 
@@ -564,12 +577,14 @@ int relcp_step(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_const
     memset(&R, 0, sizeof(R));
     const int64_t nb = b->n;
     CKS(ensure_common(ctx, nb));
+    PHASE(ctx, "step.enter");
     double t0 = now_ms();
     // W frozen at C^k; U_free (P:L557-561 / P:L522)
     CKS(op_build_W(ctx, b, ctx->W.p));
     k_ufree<<<grid_for(nb), RELCP_NT, 0, ctx->stream>>>(nb, ctx->p.dynamics, ctx->p.dt, b->vel, f_ext, ctx->W.p,
                                                         b->kinematic, ctx->ufree.p);
     CKL();
+    PHASE(ctx, "step.W_ufree");
     int64_t n0 = 0;
     nvtxRangePushA("relcp_generate");
     int rc = generate_impl(ctx, b, cs, &n0);  // Alg. 1 lines 1-2
@@ -583,7 +598,9 @@ int relcp_step(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_const
         relcp_solve_report sr;
         double ts = now_ms();
         nvtxRangePushA("relcp_solve_lcp");
+        PHASE(ctx, "solve.enter");
         rc = lcp_solve(ctx, b, cs, &sr);  // lines 3 / 10
+        PHASE(ctx, "solve.done");
         nvtxRangePop();
         R.ms_solve += now_ms() - ts;
         if (rc < 0) return rc;
@@ -621,6 +638,7 @@ int relcp_step(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_const
                                                          b->vel);
     CKL();
     CK(cudaStreamSynchronize(ctx->stream));
+    PHASE(ctx, "step.accept");
     ctx->step_nb = -1;  // bodies moved: the pair list is stale
     if (rep) *rep = R;
     if (R.status) return R.status;

@@ -9,6 +9,23 @@
 
 #include "../../include/relcp.h"
 
+// Debug build only (-DRELCP_PHASE_TIMING, tools/phases.py): synchronise and
+// print the host time since the previous mark.  Compiled out of librelcp.so.
+#ifdef RELCP_PHASE_TIMING
+#include <chrono>
+inline std::chrono::steady_clock::time_point relcp_phase_last = std::chrono::steady_clock::now();  // one per .so
+inline void relcp_phase_mark(cudaStream_t st, const char *name) {
+    auto &last = relcp_phase_last;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[phase] %-24s %9.3f ms\n", name, std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
+#define PHASE(ctx, name) relcp_phase_mark((ctx)->stream, name)
+#else
+#define PHASE(ctx, name) ((void)0)
+#endif
+
 #define RELCP_NT 256          // threads per block for streaming kernels
 #define RELCP_SM_COUNT 148    // B200
 #define RELCP_MAX_DIRS 1024   // cap on the SNSD start sample
@@ -33,6 +50,10 @@ struct DevBuf {
         p = nullptr;
         cap = 0;
     }
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() { release(); }  // relcp_destroy's `delete ctx` frees every buffer
 };
 
 // Device-side state of one LCP solve (BB projected gradient, R1).
@@ -109,6 +130,9 @@ struct relcp_ctx {
     DevBuf<double> tphi, tn, tra, trb;  // (P), (3,P) planes
     DevBuf<int> tflag, tstat;
     DevBuf<int> multi;          // pairs needing the SNSD multistart (stage 2)
+    DevBuf<int> nlist;          // ellipsoid pairs under the SNSD bound (Newton stage 1)
+    DevBuf<double> dirs;        // (3, dirs_n) multistart directions (k_dirs)
+    int dirs_n = 0;
     DevBuf<long long> scan_ll;  // scan scratch
     DevBuf<long long> scan_tmp;
     DevBuf<int> cell_count, cell_start, cell_fill, cell_items, body_cell;

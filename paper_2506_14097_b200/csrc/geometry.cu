@@ -273,10 +273,27 @@ __device__ int snsd_stage1(const double *d, const Sym &Sa, const Sym &Sb, double
     return ok ? SNSD_MULTI : -SNSD_MULTI;  // sign carries the incumbent's certification
 }
 
+// The n_dirs-point Fibonacci sphere of the stage-2 multistart, (3, n_dirs)
+// planes: m_i = (r cos(g i), r sin(g i), z), z = 1 - (2i + 1)/n, r = sqrt(1 - z^2),
+// g = pi (3 - sqrt 5).  Shared by every pair, so tabulated once per context.
+__global__ void k_dirs(int n_dirs, double *__restrict__ dirs) {
+    const double ga = 3.14159265358979323846 * (3.0 - sqrt(5.0));
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_dirs; i += gridDim.x * blockDim.x) {
+        const double z = 1.0 - (2.0 * i + 1.0) / n_dirs;
+        const double r = sqrt(fmax(0.0, 1.0 - z * z));
+        double sn, cs;
+        sincos(ga * i, &sn, &cs);
+        dirs[i] = r * cs;
+        dirs[n_dirs + i] = r * sn;
+        dirs[2 * n_dirs + i] = z;
+    }
+}
+
 // Stage 2 (overlap / touching): multistart from the best `n_dirs`-sample
 // directions against the incumbent (nb, status st_best) from stage 1.
-__device__ int snsd_stage2(const double *d, const Sym &Sa, const Sym &Sb, int n_dirs, double *nb, int st_best,
-                           double &phi, double *nout, double *ra, double *rb) {
+__device__ int snsd_stage2(const double *d, const Sym &Sa, const Sym &Sb, int n_dirs,
+                           const double *__restrict__ dirs, double *nb, int st_best, double &phi, double *nout,
+                           double *ra, double *rb) {
     const double dn = sqrt(d3(d, d));
     const double dh[3] = {d[0] / dn, d[1] / dn, d[2] / dn};
     Eval Eb;
@@ -289,13 +306,9 @@ __device__ int snsd_stage2(const double *d, const Sym &Sa, const Sym &Sb, int n_
         int topi[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) { topf[k] = -INFINITY; topi[k] = -1; }
-        const double ga = 3.14159265358979323846 * (3.0 - sqrt(5.0));
         for (int i = 0; i < n_dirs; ++i) {
-            const double z = 1.0 - (2.0 * i + 1.0) / n_dirs;
-            const double r = sqrt(fmax(0.0, 1.0 - z * z));
-            double sn, cs;
-            sincos(ga * i, &sn, &cs);
-            const double m[3] = {r * cs, r * sn, z};
+            // warp-uniform address: one broadcast load per plane
+            const double m[3] = {__ldg(dirs + i), __ldg(dirs + n_dirs + i), __ldg(dirs + 2 * n_dirs + i)};
             const double f = fval(m, d, Sa, Sb);
             if (f > topf[K - 1]) {
                 int p = K - 1;
@@ -311,11 +324,7 @@ __device__ int snsd_stage2(const double *d, const Sym &Sa, const Sym &Sb, int n_
         for (int k = 0; k < K; ++k) {
             if (topi[k] < 0) continue;
             const int i = topi[k];
-            const double z = 1.0 - (2.0 * i + 1.0) / n_dirs;
-            const double r = sqrt(fmax(0.0, 1.0 - z * z));
-            double sn, cs;
-            sincos(ga * i, &sn, &cs);
-            double m[3] = {r * cs, r * sn, z};
+            double m[3] = {dirs[i], dirs[n_dirs + i], dirs[2 * n_dirs + i]};
             Eval Em;
             int ok = newton_sphere(m, d, dn, Sa, Sb, Em);
             if (better(Em.f, m, fb, nb, dh)) {
@@ -482,22 +491,38 @@ __device__ __forceinline__ void store_pair(int64_t k, int64_t planes, double f, 
     }
 }
 
-// K3/K10 stage 1 over all pairs; pairs needing the multistart are listed
-// (list order is scheduling dependent, the per-pair results are not).
-__global__ void __launch_bounds__(128) k_snsd_stage1(int64_t np, const int *__restrict__ pi,
+// Append k to a device list when `push`, one atomic per warp (the list order
+// is scheduling dependent; every consumer's per-pair result is not).
+__device__ __forceinline__ void list_push(bool push, int64_t k, int *list, unsigned *count) {
+    const unsigned act = __activemask();
+    const unsigned bal = __ballot_sync(act, push);
+    if (!bal) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(act) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(count, (unsigned)__popc(bal));
+    base = __shfl_sync(act, base, leader);
+    if (push) list[base + __popc(bal & ((1u << lane) - 1u))] = (int)k;
+}
+
+// K3/K10 stage 0 over all pairs: spherocylinder / torus / mixed pairs in full;
+// ellipsoid pairs get the lower bound Phi >= F(d/|d|) (snsd_stage1) and, when
+// it does not reject them, go to the Newton list, so that the Newton stage
+// runs with full warps (most pairs of a check are rejected by the bound).
+__global__ void __launch_bounds__(128) k_snsd_stage0(int64_t np, const int *__restrict__ pi,
                                                      const int *__restrict__ pj, const double *__restrict__ pos,
                                                      const double *__restrict__ Sig, Box3 box, double reject_above,
                                                      double *__restrict__ phi, double *__restrict__ nrm,
                                                      double *__restrict__ ra, double *__restrict__ rb,
-                                                     int *__restrict__ status, int64_t planes, int *multi,
-                                                     unsigned *n_multi, const int32_t *__restrict__ shape,
+                                                     int *__restrict__ status, int64_t planes, int *nlist,
+                                                     unsigned *n_nlist, const int32_t *__restrict__ shape,
                                                      const double *__restrict__ axes) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < np; k += (int64_t)gridDim.x * blockDim.x) {
         double d[3];
         Sym Sa, Sb;
         pair_geom(k, pi, pj, pos, Sig, box, d, Sa, Sb);
         double f, n[3], r1[3], r2[3];
-        int st;
+        int st = -1;  // >= 0: outputs final here; -1: bound (phi only) or Newton list
+        bool newton = false;
         const int sha = shape ? shape[pi[k]] : 0, shb = shape ? shape[pj[k]] : 0;
         if (sha == RELCP_SHAPE_SPHEROCYLINDER && shb == RELCP_SHAPE_SPHEROCYLINDER) {
             const double ga[6] = {Sa.xx, Sa.xy, Sa.xz, Sa.yy, Sa.yz, Sa.zz};
@@ -513,15 +538,53 @@ __global__ void __launch_bounds__(128) k_snsd_stage1(int64_t np, const int *__re
             for (int c = 0; c < 3; ++c) n[c] = r1[c] = r2[c] = nan("");
             st = SNSD_DEGENERATE;
         } else {
-            st = snsd_stage1(d, Sa, Sb, reject_above, f, n, r1, r2);
+            const double dn = sqrt(d3(d, d));
+            if (!(dn >= 1e-12)) {
+                f = nan("");
+                for (int c = 0; c < 3; ++c) n[c] = r1[c] = r2[c] = nan("");
+                st = SNSD_DEGENERATE;
+            } else {
+                const double nb[3] = {d[0] / dn, d[1] / dn, d[2] / dn};
+                f = fval(nb, d, Sa, Sb);
+                if (f >= reject_above + 1e-12 * fmax(1.0, dn)) {
+                    // phi = the bound; only phi and the status are consumed (k_flag)
+                    phi[k] = f;
+                    status[k] = SNSD_BOUND;
+                } else {
+                    newton = true;
+                }
+            }
         }
-        store_pair(k, planes, f, n, r1, r2, phi, nrm, ra, rb);
-        if (st == SNSD_MULTI || st == -SNSD_MULTI) {
-            multi[atomicAdd(n_multi, 1u)] = (int)k;
-            status[k] = st == SNSD_MULTI ? SNSD_OK : SNSD_NONCONV;  // incumbent's certification
-        } else {
+        list_push(newton, k, nlist, n_nlist);
+        if (st >= 0) {
+            store_pair(k, planes, f, n, r1, r2, phi, nrm, ra, rb);
             status[k] = st;
         }
+    }
+}
+
+// Stage 1 over the Newton list (ellipsoid pairs under the bound): Newton from
+// d/|d|; pairs needing the multistart are listed for stage 2.
+__global__ void __launch_bounds__(128) k_snsd_stage1(const int *__restrict__ nlist, const unsigned *__restrict__ n_nlist,
+                                                     const int *__restrict__ pi, const int *__restrict__ pj,
+                                                     const double *__restrict__ pos, const double *__restrict__ Sig,
+                                                     Box3 box, double *__restrict__ phi, double *__restrict__ nrm,
+                                                     double *__restrict__ ra, double *__restrict__ rb,
+                                                     int *__restrict__ status, int64_t planes, int *multi,
+                                                     unsigned *n_multi) {
+    const int64_t m = *n_nlist;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = nlist[i];
+        double d[3];
+        Sym Sa, Sb;
+        pair_geom(k, pi, pj, pos, Sig, box, d, Sa, Sb);
+        double f, n[3], r1[3], r2[3];
+        // reject_above = +inf: the bound was tested in stage 0
+        const int st = snsd_stage1(d, Sa, Sb, INFINITY, f, n, r1, r2);
+        store_pair(k, planes, f, n, r1, r2, phi, nrm, ra, rb);
+        const bool mult = st == SNSD_MULTI || st == -SNSD_MULTI;
+        list_push(mult, k, multi, n_multi);
+        status[k] = mult ? (st == SNSD_MULTI ? SNSD_OK : SNSD_NONCONV) : st;  // incumbent's certification
     }
 }
 
@@ -529,7 +592,8 @@ __global__ void __launch_bounds__(128) k_snsd_stage1(int64_t np, const int *__re
 __global__ void __launch_bounds__(128) k_snsd_stage2(const int *__restrict__ multi, const unsigned *__restrict__ n_multi,
                                                      const int *__restrict__ pi, const int *__restrict__ pj,
                                                      const double *__restrict__ pos, const double *__restrict__ Sig,
-                                                     Box3 box, int n_dirs, double *__restrict__ phi,
+                                                     Box3 box, int n_dirs, const double *__restrict__ dirs,
+                                                     double *__restrict__ phi,
                                                      double *__restrict__ nrm, double *__restrict__ ra,
                                                      double *__restrict__ rb, int *__restrict__ status,
                                                      int64_t planes) {
@@ -541,7 +605,7 @@ __global__ void __launch_bounds__(128) k_snsd_stage2(const int *__restrict__ mul
         pair_geom(k, pi, pj, pos, Sig, box, d, Sa, Sb);
         double nb[3] = {nrm[k], nrm[planes + k], nrm[2 * planes + k]};
         double f, n[3], r1[3], r2[3];
-        const int st = snsd_stage2(d, Sa, Sb, n_dirs, nb, status[k], f, n, r1, r2);
+        const int st = snsd_stage2(d, Sa, Sb, n_dirs, dirs, nb, status[k], f, n, r1, r2);
         store_pair(k, planes, f, n, r1, r2, phi, nrm, ra, rb);
         status[k] = st;
     }
@@ -556,14 +620,26 @@ int geo_snsd(relcp_ctx *ctx, int64_t np, const int *pi, const int *pj, const dou
     int nd = ctx->p.n_dirs > 0 ? ctx->p.n_dirs : 256;
     if (nd > RELCP_MAX_DIRS) nd = RELCP_MAX_DIRS;
     CK(ctx->multi.grow(np));
-    CK(cudaMemsetAsync(ctx->counter.p + 1, 0, sizeof(unsigned), ctx->stream));
+    CK(ctx->nlist.grow(np));
+    if (ctx->dirs_n != nd) {
+        CK(ctx->dirs.grow(3 * nd));
+        k_dirs<<<(nd + 127) / 128, 128, 0, ctx->stream>>>(nd, ctx->dirs.p);
+        CKL();
+        ctx->dirs_n = nd;
+    }
+    // counter[1] = stage-2 list length, counter[2] = Newton list length
+    CK(cudaMemsetAsync(ctx->counter.p + 1, 0, 2 * sizeof(unsigned), ctx->stream));
     int64_t g = (np + 127) / 128;
     if (g > 148 * 64) g = 148 * 64;
-    k_snsd_stage1<<<(unsigned)g, 128, 0, ctx->stream>>>(np, pi, pj, pos, Sig, bx, reject_above, phi, nrm, ra, rb,
-                                                        status, planes, ctx->multi.p, ctx->counter.p + 1, shape,
+    k_snsd_stage0<<<(unsigned)g, 128, 0, ctx->stream>>>(np, pi, pj, pos, Sig, bx, reject_above, phi, nrm, ra, rb,
+                                                        status, planes, ctx->nlist.p, ctx->counter.p + 2, shape,
                                                         axes);
     CKL();
-    k_snsd_stage2<<<148 * 8, 128, 0, ctx->stream>>>(ctx->multi.p, ctx->counter.p + 1, pi, pj, pos, Sig, bx, nd, phi,
+    k_snsd_stage1<<<148 * 8, 128, 0, ctx->stream>>>(ctx->nlist.p, ctx->counter.p + 2, pi, pj, pos, Sig, bx, phi, nrm,
+                                                    ra, rb, status, planes, ctx->multi.p, ctx->counter.p + 1);
+    CKL();
+    k_snsd_stage2<<<148 * 8, 128, 0, ctx->stream>>>(ctx->multi.p, ctx->counter.p + 1, pi, pj, pos, Sig, bx, nd,
+                                                    ctx->dirs.p, phi,
                                                     nrm, ra, rb, status, planes);
     CKL();
     return RELCP_OK;
@@ -712,6 +788,7 @@ int geo_broadphase(relcp_ctx *ctx, int64_t nb, const double *pos, const double *
     CKL();
     CK(cudaMemcpyAsync(ctx->red_host, ctx->red.p, 7 * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    PHASE(ctx, "bp.bounds");
     double lo[3], hi[3], rmax = ctx->red_host[6];
     for (int k = 0; k < 3; ++k) {
         lo[k] = ctx->red_host[k];
@@ -757,6 +834,7 @@ int geo_broadphase(relcp_ctx *ctx, int64_t nb, const double *pos, const double *
     k_cell_fill<<<grid_for(nb), RELCP_NT, 0, st>>>(nb, ctx->body_cell.p, ctx->cell_start.p, ctx->cell_fill.p,
                                                     ctx->cell_items.p);
     CKL();
+    PHASE(ctx, "bp.cells");
     const int gp = grid_for(nb, 128, 32);
     k_pairs2<0><<<gp, 128, 0, st>>>(nb, pos, rad, G, margin, ctx->body_cell.p, ctx->cell_start.p, ctx->cell_count.p,
                                     ctx->cell_items.p, ctx->pair_cnt.p, nullptr, nullptr);
@@ -765,11 +843,13 @@ int geo_broadphase(relcp_ctx *ctx, int64_t nb, const double *pos, const double *
     long long total = 0;
     CK(ctx->scan_ll.grow(nb + 1));
     CKS(scan_exclusive_ll(ctx, ctx->pair_cnt.p, ctx->scan_ll.p, nb + 1, &total));
+    PHASE(ctx, "bp.count_scan");
     CK(ctx->pi.grow(total > 0 ? total : 1));
     CK(ctx->pj.grow(total > 0 ? total : 1));
     k_pairs2<1><<<gp, 128, 0, st>>>(nb, pos, rad, G, margin, ctx->body_cell.p, ctx->cell_start.p, ctx->cell_count.p,
                                     ctx->cell_items.p, ctx->scan_ll.p, ctx->pi.p, ctx->pj.p);
     CKL();
     ctx->npairs = total;
+    PHASE(ctx, "bp.pairs");
     return RELCP_OK;
 }

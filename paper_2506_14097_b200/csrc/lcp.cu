@@ -247,6 +247,7 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
     const int64_t nc = cs->count, nb = b->n;
     if (!cs->q || !cs->lambda || !cs->g) return set_err(ctx, RELCP_E_ARG, "solve: q, lambda and g are required");
     if (ctx->op_nc != nc || ctx->op_nb != nb || ctx->op_key_ia != cs->ia) CKS(op_prepare(ctx, b, cs));
+    PHASE(ctx, "solve.prepare");
     CK(ctx->vtmp.grow(nc > 0 ? nc : 1));
     const double s = op_scale(ctx);
     cudaStream_t st = ctx->stream;
@@ -269,6 +270,7 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
         CKS(op_scatter(ctx, nb, ctx->vtmp.p, nullptr, 0, &ctx->st.p->pnorm, ctx->U.p, nullptr));
         CKS(op_gather_apply(ctx, cs, ctx->U.p, ctx->vtmp.p, s, 1));
     }
+    PHASE(ctx, "solve.power");
     // g_0 = A x_0 + q
     CKS(op_scatter(ctx, nb, cs->lambda, nullptr, 0, nullptr, ctx->U.p, nullptr));
     k_lcp_init<<<gridc, RELCP_NT, 0, st>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->U.p, s, cs->q,
@@ -297,6 +299,7 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
         k_apgd_setup<<<1, 1, 0, st>>>(ctx->st.p);
         CKL();
     }
+    PHASE(ctx, "solve.init");
     int batch = ctx->p.check_every > 0 ? ctx->p.check_every : 32;
     if (ctx->timing) {
         if (batch > 64) batch = 64;
@@ -394,6 +397,7 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
         ++batches;
         pending = batch;
     }
+    PHASE(ctx, "solve.loop");
     if (gexec) CK(cudaGraphExecDestroy(gexec));
     if (apgd && ctx->st_host->par) {  // the current APGD iterate lives in the second buffer
         CK(cudaMemcpyAsync(cs->lambda, xB, sizeof(double) * nc, cudaMemcpyDeviceToDevice, st));
