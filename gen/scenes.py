@@ -118,6 +118,22 @@ def cfg1(seed: int = 1) -> dict:
                       dynamics=INERTIAL, name="cfg1")
 
 
+def cfg1_relaxed(dt: float = 1e-3, vel_seed: int = 11) -> dict:
+    """the cfg1 bodies at the overlap-free state in
+    tests/golden/cfg1_relaxed.txt (written by tools/make_relaxed.py, which runs
+    the ORACLE's overdamped relaxation), with fresh u, w ~ N(0, 1) drawn from
+    PCG64(vel_seed); inertial, time step `dt` (1e-3 = cfg1; 0.1 = cfg1-bigdt).
+    This function only reads the stored state and draws velocities."""
+    import os
+    sc = cfg1()
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                        "cfg1_relaxed.txt")
+    st = np.loadtxt(path, comments="#")
+    sc.update(pos=st[:, :3].copy(), quat=st[:, 3:7].copy(), dt=float(dt), name=f"cfg1-relaxed-dt{dt:g}",
+              vel=np.random.Generator(np.random.PCG64(vel_seed)).standard_normal((sc["n"], 6)))
+    return sc
+
+
 def cfg2(seed: int = 2, n: int = 20000) -> dict:
     return suspension(n, None, 0.40, seed, dt=1e-2, dynamics=OVERDAMPED,
                       velocities=False, shape_fn=_cfg2_shape, name="cfg2")

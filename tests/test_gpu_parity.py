@@ -369,6 +369,20 @@ def test_step_parity_overdamped_cfg2_recipe(orc, R):
     assert rep["status"] == R.W_RECURSION_CAP
 
 
+def test_step_parity_cfg1_relaxed(orc, R):
+    """cfg1-relaxed (overlap-free start): both sides stop after
+    the recursion-0 solve (reduction corollary)."""
+    r, rep, _ = _compare_step(orc, R, scenes.cfg1_relaxed())
+    assert rep["recursions"] == 0 and rep["max_overlap"] <= 1e-5
+
+
+def test_step_parity_cfg1_bigdt(orc, R):
+    """cfg1-bigdt: the relaxed start at dt = 0.1 augments several times; the
+    appended rows, generations and the accepted state match the oracle."""
+    r, rep, _ = _compare_step(orc, R, scenes.cfg1_relaxed(dt=0.1))
+    assert rep["recursions"] >= 1 and rep["status"] == 0
+
+
 def test_step_parity_bigdt_augments(orc, R):
     sc = scenes.suspension(300, (1.0, 0.6, 0.4), 0.3, 9, dt=2e-2)
     r, rep, _ = _compare_step(orc, R, sc, max_recursions=2)
