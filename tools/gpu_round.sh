@@ -9,5 +9,5 @@ export RELCP_PROFILE_TIMED=1
 timeout 400 $CMD > gpurun_out/plain.json 2> gpurun_out/plain.err && \
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo ncu1_rc=$?
 unset RELCP_PROFILE_TIMED
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_scatter|k_lcp_iter|k_gather" -s 60 -c 4 -o gpurun_out/prof_iter python tools/kbench.py 2000000 200 > gpurun_out/ncu_full.log 2>&1; echo ncu2_rc=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_scatter|k_lcp_iter" -s 100 -c 4 -o gpurun_out/prof_iter python tools/kbench.py 2000000 200 > gpurun_out/ncu_full.log 2>&1; echo ncu2_rc=$?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_snsd" -c 3 -o gpurun_out/prof_snsd python tools/kbench.py 2000000 20 > gpurun_out/ncu_snsd.log 2>&1; echo ncu3_rc=$?
