@@ -103,3 +103,45 @@ def test_invalid_params_refused(R):
     ctx = R.Context()
     with pytest.raises(R.RelcpError):
         ctx.set_params(max_recursions=1000)
+
+
+def test_generate_capacity_error_reports_size(R):
+    """A_0 larger than the store: E_CAPACITY with the required row count in
+    `count` (include/relcp.h), nothing written past capacity."""
+    sc = scenes.cfg1()
+    ctx = R.Context(dt=sc["dt"], box=list(sc["box"]))
+    bodies = R.BodyState.from_scene(sc)
+    cs = R.ConstraintStore(16)
+    guard = cs.ia.clone()
+    with pytest.raises(R.RelcpError) as e:
+        ctx.generate_contacts(bodies, cs)
+    assert e.value.code == R.E_CAPACITY and cs.count > 16
+    assert torch.equal(cs.ia, guard)
+
+
+def test_nan_input_is_refused(R):
+    """A NaN in q: the solve stops with E_NAN instead of iterating on NaNs."""
+    sc = scenes.cfg1()
+    ctx = R.Context(dt=sc["dt"], box=list(sc["box"]))
+    bodies = R.BodyState.from_scene(sc)
+    cs = R.ConstraintStore(4000)
+    ctx.generate_contacts(bodies, cs)
+    cs.q[3] = float("nan")
+    with pytest.raises(R.RelcpError) as e:
+        ctx.solve_lcp(bodies, cs)
+    assert e.value.code == R.E_NAN
+
+
+@pytest.mark.parametrize("solver", [0, 1, 2])
+def test_iteration_cap_returns_warning(R, solver):
+    """lcp_max_iter reached: W_MAX_ITER (> 0, not an error), exactly the cap
+    executed, the last iterate returned projected (lambda >= 0)."""
+    sc = scenes.cfg5(n=1000)  # its A_0 needs ~150 BB iterations at 1e-8
+    ctx = R.Context(dt=sc["dt"], box=list(sc["box"]), lcp_tol=1e-14, lcp_max_iter=37, solver=solver)
+    bodies = R.BodyState.from_scene(sc)
+    cs = R.ConstraintStore(4000)
+    ctx.generate_contacts(bodies, cs)
+    rep = ctx.solve_lcp(bodies, cs)
+    assert rep["status"] == R.W_MAX_ITER and not rep["converged"]
+    assert rep["iterations"] == 37 and rep["residual"] > 1e-14
+    assert bool((cs.lam[:cs.count] >= 0).all())

@@ -175,6 +175,26 @@ def test_lcp_solve_parity_cfg1(orc, R, cfg1_a0, solver):
 
 
 @pytest.mark.parametrize("solver", [0, 1, 2])
+def test_lcp_solve_parity_shuffled_store(orc, R, cfg1_a0, solver):
+    """A caller's store in arbitrary row order (general CSR path: both sides
+    in the CSR, K6 SORTED = false; the fused solver falls back to APGD): same
+    solution as the oracle, row for row."""
+    sc, r = cfg1_a0
+    c = r["constraints"]
+    perm = np.random.default_rng(17).permutation(len(c["ia"]))
+    ctx = _ctx(R, sc, lcp_tol=1e-10, solver=solver, lcp_max_iter=2_000_000)
+    bodies = R.BodyState.from_scene(sc)
+    cs = R.ConstraintStore.from_rows(c["ia"][perm], c["ib"][perm], c["n"][perm], c["ta"][perm], c["tb"][perm],
+                                     q=r["q_hist"][0][perm])
+    rep = ctx.solve_lcp(bodies, cs)
+    assert rep["converged"] and rep["residual"] <= 1e-10
+    lam = cs.lam[:cs.count].cpu().numpy()
+    lam_ref = c["lam"][perm]
+    assert np.max(np.abs(lam - lam_ref)) <= 1e-6 * np.max(np.abs(lam_ref))
+    assert abs(rep["objective"] - r["f"][0]) <= 1e-6 * abs(r["f"][0])
+
+
+@pytest.mark.parametrize("solver", [0, 1, 2])
 @pytest.mark.parametrize("seed", [0, 1, 2])
 def test_lcp_vs_enumeration_tiny(orc, R, seed, solver):
     """Tiny random LCPs: the GPU solution equals the brute-force support
