@@ -95,6 +95,9 @@ struct relcp_ctx {
     int op_sorted = 0;               // store sorted by ia: a-side read from the store (K6)
     int64_t op_cap = 0;              // store plane stride
     const double *op_n = nullptr, *op_ta = nullptr;
+    int64_t op_rs = 0;               // compact row plane stride (= op_nc)
+    DevBuf<double> rc;               // (6, op_nc) compact rows (rows.cuh), for the row passes
+    int op_compact = 0;              // every row has t . n ~ 0: row passes read rc
     DevBuf<int> pa;                  // (nb + 1) a-side row pointer of a sorted store
     DevBuf<int> mi;                  // merge scratch (3, rows)
     DevBuf<double> md;               // merge scratch (13, rows)

@@ -16,9 +16,13 @@
 #include "reduce.cuh"
 
 #include "rows.cuh"
-#define row_dot_l row_dot_u
+// row . [U_a; U_b]: compact planes when the operator holds them (CR), else the store
+#define ROW_DOT(a) (CR ? row_dot_c((a), rs, ia, ib, rc, U) : row_dot_u((a), cap, ia, ib, n, ta, tb, U))
 #ifndef ITER_MINB
 #define ITER_MINB 4  // resident K7 blocks per SM (register budget); grid = 148 * ITER_MINB
+#endif
+#ifndef ITER_MINB_CR
+#define ITER_MINB_CR 3  // with compact rows (decode registers): same-box A/B 113 us vs 124 us at 4 with spills
 #endif
 #ifndef ITER_ILP
 #define ITER_ILP 2   // rows per thread per trip in K7
@@ -53,9 +57,11 @@ __global__ void k_state_init(LcpState *st, int64_t nc, double tol, long long max
 }
 
 // g = s D^T U + q for the (projected) warm start; r_0; alpha_0 = 1/L.
+template <bool CR>
 __global__ void __launch_bounds__(RELCP_NT) k_lcp_init(int64_t nc, int64_t cap, const int32_t *__restrict__ ia,
                                                        const int32_t *__restrict__ ib, const double *__restrict__ n,
                                                        const double *__restrict__ ta, const double *__restrict__ tb,
+                                                       int64_t rs, const double *__restrict__ rc,
                                                        const double *__restrict__ U, double s,
                                                        const double *__restrict__ q, const double *__restrict__ x,
                                                        double *__restrict__ g, double *part, unsigned *counter,
@@ -63,7 +69,7 @@ __global__ void __launch_bounds__(RELCP_NT) k_lcp_init(int64_t nc, int64_t cap, 
     __shared__ double sh[64];
     double acc[2] = {0.0, 0.0};
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
-        double gv = fma(s, row_dot_l(a, cap, ia, ib, n, ta, tb, U), q[a]);
+        double gv = fma(s, ROW_DOT(a), q[a]);
         g[a] = gv;
         acc[0] = fmax(acc[0], fabs(fmin(x[a], gv)));
         acc[1] = fmax(acc[1], isfinite(gv) ? 0.0 : 1.0);
@@ -88,9 +94,11 @@ __global__ void __launch_bounds__(RELCP_NT) k_lcp_init(int64_t nc, int64_t cap, 
 }
 
 // One BB projected-gradient update (the gather half of iteration k).
-__global__ void __launch_bounds__(RELCP_NT, ITER_MINB) k_lcp_iter(int64_t nc, int64_t cap, const int32_t *__restrict__ ia,
+template <bool CR>
+__global__ void __launch_bounds__(RELCP_NT, CR ? ITER_MINB_CR : ITER_MINB) k_lcp_iter(int64_t nc, int64_t cap, const int32_t *__restrict__ ia,
                                                        const int32_t *__restrict__ ib, const double *__restrict__ n,
                                                        const double *__restrict__ ta, const double *__restrict__ tb,
+                                                       int64_t rs, const double *__restrict__ rc,
                                                        const double *__restrict__ U, double s,
                                                        const double *__restrict__ q, double *__restrict__ x,
                                                        double *__restrict__ g, double *part, unsigned *counter,
@@ -111,7 +119,7 @@ __global__ void __launch_bounds__(RELCP_NT, ITER_MINB) k_lcp_iter(int64_t nc, in
             xo[u] = x[ac];
             go[u] = g[ac];
             qv[u] = q[ac];
-            rd[u] = row_dot_l(ac, cap, ia, ib, n, ta, tb, U);
+            rd[u] = ROW_DOT(ac);
         }
 #pragma unroll
         for (int u = 0; u < ITER_ILP; ++u) {
@@ -166,10 +174,11 @@ __global__ void __launch_bounds__(RELCP_NT, ITER_MINB) k_lcp_iter(int64_t nc, in
 //   theta+ = (theta sqrt(theta^2 + 4) - theta^2) / 2,
 //   beta+  = theta (1 - theta) / (theta^2 + theta+).
 // The new iterate overwrites the previous one's slot; the parity bit flips.
-__global__ void __launch_bounds__(RELCP_NT, ITER_MINB) k_apgd_iter(
+template <bool CR>
+__global__ void __launch_bounds__(RELCP_NT, CR ? ITER_MINB_CR : ITER_MINB) k_apgd_iter(
     int64_t nc, int64_t cap, const int32_t *__restrict__ ia, const int32_t *__restrict__ ib,
-    const double *__restrict__ n, const double *__restrict__ ta, const double *__restrict__ tb,
-    const double *__restrict__ U, double s, const double *__restrict__ q, double *xA, double *gA, double *xB,
+    const double *__restrict__ n, const double *__restrict__ ta, const double *__restrict__ tb, int64_t rs,
+    const double *__restrict__ rc, const double *__restrict__ U, double s, const double *__restrict__ q, double *xA, double *gA, double *xB,
     double *gB, double *part, unsigned *counter, LcpState *st) {
     __shared__ double sh[3 * 32];
     if (st->done) return;
@@ -183,7 +192,7 @@ __global__ void __launch_bounds__(RELCP_NT, ITER_MINB) k_apgd_iter(
         const double x0 = xc[a], g0 = gc[a];
         const double y = x0 + beta * (x0 - xp[a]), gy = g0 + beta * (g0 - gp[a]);
         const double xn = fmax(0.0, y - t * gy);
-        const double gn = fma(s, row_dot_l(a, cap, ia, ib, n, ta, tb, U), q[a]);
+        const double gn = fma(s, ROW_DOT(a), q[a]);
         xp[a] = xn;
         gp[a] = gn;
         acc[0] = fma(gy, xn - x0, acc[0]);
@@ -273,8 +282,15 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
     PHASE(ctx, "solve.power");
     // g_0 = A x_0 + q
     CKS(op_scatter(ctx, nb, cs->lambda, nullptr, 0, nullptr, ctx->U.p, nullptr));
-    k_lcp_init<<<gridc, RELCP_NT, 0, st>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->U.p, s, cs->q,
-                                           cs->lambda, cs->g, ctx->partials.p, ctx->counter.p, ctx->st.p);
+    const bool cr = ctx->op_compact != 0;
+    const int gridi = cr ? grid_for(nc, RELCP_NT, ITER_MINB_CR) : gridc;  // iteration kernels: one wave
+#define ROWS_ARGS nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->op_rs, ctx->rc.p
+    if (cr)
+        k_lcp_init<true><<<gridc, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g, ctx->partials.p,
+                                                     ctx->counter.p, ctx->st.p);
+    else
+        k_lcp_init<false><<<gridc, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g,
+                                                      ctx->partials.p, ctx->counter.p, ctx->st.p);
     CKL();
     const bool apgd = ctx->p.solver == RELCP_SOLVER_APGD || (ctx->p.solver == RELCP_SOLVER_APGD_FUSED && !ctx->op_sorted);
     // fused APGD needs the sorted store (a-side rows contiguous); else plain APGD
@@ -329,14 +345,18 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
             if (ev_on) CK(cudaEventRecord(ctx->ev[3 * j], st));
             CKS(op_scatter(ctx, nb, cs->lambda, cs->g, apgd ? 2 : 1, nullptr, ctx->U.p, nullptr, xB, gB));
             if (ev_on) CK(cudaEventRecord(ctx->ev[3 * j + 1], st));
-            if (apgd)
-                k_apgd_iter<<<gridc, RELCP_NT, 0, st>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb,
-                                                        ctx->U.p, s, cs->q, cs->lambda, cs->g, xB, gB,
-                                                        ctx->partials.p, ctx->counter.p, ctx->st.p);
+            if (apgd && cr)
+                k_apgd_iter<true><<<gridi, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g, xB,
+                                                              gB, ctx->partials.p, ctx->counter.p, ctx->st.p);
+            else if (apgd)
+                k_apgd_iter<false><<<gridi, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g, xB,
+                                                               gB, ctx->partials.p, ctx->counter.p, ctx->st.p);
+            else if (cr)
+                k_lcp_iter<true><<<gridi, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g,
+                                                             ctx->partials.p, ctx->counter.p, ctx->st.p);
             else
-                k_lcp_iter<<<gridc, RELCP_NT, 0, st>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb,
-                                                       ctx->U.p, s, cs->q, cs->lambda, cs->g, ctx->partials.p,
-                                                       ctx->counter.p, ctx->st.p);
+                k_lcp_iter<false><<<gridi, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g,
+                                                              ctx->partials.p, ctx->counter.p, ctx->st.p);
             CKL();
             if (ev_on) CK(cudaEventRecord(ctx->ev[3 * j + 2], st));
         }

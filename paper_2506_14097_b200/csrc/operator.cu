@@ -24,6 +24,7 @@
 //   * k_fused_rows: the fused-APGD row pass (lcp.cu solver 2).
 #include "common.cuh"
 #include "reduce.cuh"
+#include "rows.cuh"
 
 #ifndef SCATTER_WPB
 #define SCATTER_WPB 4    // warps per block (same-box A/B: 4 x 8 blocks beats 8 x 4)
@@ -141,6 +142,38 @@ __global__ void k_payload(int64_t E, int64_t cap, const double *__restrict__ n, 
     }
 }
 
+// Compact rows (rows.cuh) for the constraint-major row passes (K7, the apply
+// gather): n, t_a, t_b -> 6 planes, stride rs.  The encoding assumes t . n = 0
+// (t = r x n); a row with |t . n| > 1e-13 (1 + |t|) sets *nonorth and
+// the operator keeps reading the full rows.
+__global__ void k_compact(int64_t nc, int64_t cap, const double *__restrict__ n, const double *__restrict__ ta,
+                          const double *__restrict__ tb, int64_t rs, double *__restrict__ rc, int *nonorth) {
+    bool bad = false;
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
+        const double nv[3] = {n[a], n[cap + a], n[2 * cap + a]};
+        const double tav[3] = {ta[a], ta[cap + a], ta[2 * cap + a]};
+        const double tbv[3] = {tb[a], tb[cap + a], tb[2 * cap + a]};
+        double u, v;
+        oct_encode(nv[0], nv[1], nv[2], u, v);
+        const CNormal c = cn_decode(u, v);
+        double a1, a2, b1, b2;
+        t_pick(c, tav, a1, a2);
+        t_pick(c, tbv, b1, b2);
+        rc[a] = u;
+        rc[rs + a] = v;
+        rc[2 * rs + a] = a1;
+        rc[3 * rs + a] = a2;
+        rc[4 * rs + a] = b1;
+        rc[5 * rs + a] = b2;
+        const double da = fabs(tav[0] * nv[0] + tav[1] * nv[1] + tav[2] * nv[2]);
+        const double db = fabs(tbv[0] * nv[0] + tbv[1] * nv[1] + tbv[2] * nv[2]);
+        const double la = sqrt(tav[0] * tav[0] + tav[1] * tav[1] + tav[2] * tav[2]);
+        const double lb = sqrt(tbv[0] * tbv[0] + tbv[1] * tbv[1] + tbv[2] * tbv[2]);
+        bad |= !(da <= 1e-13 * (1.0 + la)) || !(db <= 1e-13 * (1.0 + lb));
+    }
+    if (__any_sync(__activemask(), bad) && (threadIdx.x & 31) == 0) atomicOr(nonorth, 1);
+}
+
 int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *cs) {
     if (!b || !cs || b->n <= 0) return set_err(ctx, RELCP_E_ARG, "prepare: empty bodies");
     const int64_t nb = b->n, nc = cs->count, E = 2 * nc;
@@ -149,29 +182,34 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
     CK(ctx->W.grow(RELCP_WSTRIDE * nb));
     CK(ctx->row_ptr.grow(nb + 1));
     CK(ctx->deg.grow(nb + 1));
-    CK(ctx->fill.grow(nb + 1));
+    CK(ctx->fill.grow(nb + 2));
     CK(ctx->U.grow(6 * nb));
     CK(ctx->ecid.grow(E > 0 ? E : 1));
     CK(ctx->ew.grow(6 * (E > 0 ? E : 1)));
     CK(ctx->pa.grow(nb + 1));
+    CK(ctx->rc.grow(6 * (nc > 0 ? nc : 1)));
     CKS(op_build_W(ctx, b, ctx->W.p));
     int sorted = 0;
     CKS(store_is_sorted_by_ia(ctx, cs, &sorted));
     CK(cudaMemsetAsync(ctx->deg.p, 0, sizeof(int) * (nb + 1), ctx->stream));
     CK(cudaMemsetAsync(ctx->pa.p, 0, sizeof(int) * (nb + 1), ctx->stream));
-    CK(cudaMemsetAsync(ctx->fill.p, 0, sizeof(int) * (nb + 1), ctx->stream));  // fill[nb] = bad flag
+    CK(cudaMemsetAsync(ctx->fill.p, 0, sizeof(int) * (nb + 2), ctx->stream));  // fill[nb] bad, [nb+1] non-orthogonal
     if (nc > 0) {
         k_degree<<<grid_for(nc), RELCP_NT, 0, ctx->stream>>>(nc, cs->ia, cs->ib, sorted ? ctx->pa.p : ctx->deg.p,
                                                              ctx->deg.p, nb, ctx->fill.p + nb);
+        CKL();
+        k_compact<<<grid_for(nc), RELCP_NT, 0, ctx->stream>>>(nc, cs->capacity, cs->n, cs->ta, cs->tb, nc, ctx->rc.p,
+                                                              ctx->fill.p + nb + 1);
         CKL();
     }
     int total = 0;
     CKS(scan_exclusive_int(ctx, ctx->deg.p, ctx->row_ptr.p, nb + 1, &total));  // deg[nb] = 0
     if (sorted) CKS(scan_exclusive_int(ctx, ctx->pa.p, ctx->pa.p, nb + 1, nullptr));  // in place
-    int bad = 0;
-    CK(cudaMemcpyAsync(&bad, ctx->fill.p + nb, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    int flags[2] = {0, 0};
+    CK(cudaMemcpyAsync(flags, ctx->fill.p + nb, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    if (bad) return set_err(ctx, RELCP_E_ARG, "prepare: body index out of range or ia == ib");
+    if (flags[0]) return set_err(ctx, RELCP_E_ARG, "prepare: body index out of range or ia == ib");
+    ctx->op_compact = nc > 0 && !flags[1];
     const int64_t Ee = sorted ? nc : E;  // CSR entries: b-side only when sorted
     if (nc > 0) {
         CK(cudaMemsetAsync(ctx->fill.p, 0, sizeof(int) * nb, ctx->stream));
@@ -186,6 +224,7 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
     }
     ctx->op_sorted = sorted;
     ctx->op_cap = cs->capacity;
+    ctx->op_rs = nc;
     ctx->op_n = cs->n;
     ctx->op_ta = cs->ta;
     ctx->op_nc = nc;
@@ -505,13 +544,19 @@ int op_fused_rows(relcp_ctx *ctx, const relcp_constraints *cs, int64_t nb, doubl
 
 // ------------------------------------------------------------ gather
 #ifndef GATHER_ILP
-#define GATHER_ILP 4  // rows per thread per trip in the apply gather (independent loads in flight)
+#define GATHER_ILP 2  // rows per thread per trip in the apply gather (same-box A/B with compact rows: 2 beats 4)
+#endif
+#ifndef GATHER_MINB_CR
+#define GATHER_MINB_CR 3  // resident blocks per SM with compact rows (register budget 80)
 #endif
 
 // y = scale * D^T U ; optionally the grid-wide ||y||^2 -> st->pnorm = 1/||y||, st->L = ||y||
-__global__ void __launch_bounds__(RELCP_NT) k_gather(int64_t nc, int64_t cap, const int32_t *__restrict__ ia,
+// CR: rows from the compact planes rc (stride rs) instead of the store.
+template <bool CR>
+__global__ void __launch_bounds__(RELCP_NT, CR ? GATHER_MINB_CR : 4) k_gather(int64_t nc, int64_t cap, const int32_t *__restrict__ ia,
                                                      const int32_t *__restrict__ ib, const double *__restrict__ n,
                                                      const double *__restrict__ ta, const double *__restrict__ tb,
+                                                     int64_t rs, const double *__restrict__ rc,
                                                      const double *__restrict__ U, double scale,
                                                      double *__restrict__ y, int norm2, double *part,
                                                      unsigned *counter, LcpState *st) {
@@ -523,7 +568,8 @@ __global__ void __launch_bounds__(RELCP_NT) k_gather(int64_t nc, int64_t cap, co
 #pragma unroll
         for (int u = 0; u < GATHER_ILP; ++u) {
             const int64_t a = a0 + u * stride;
-            v[u] = scale * row_dot(a < nc ? a : a0, cap, ia, ib, n, ta, tb, U);
+            const int64_t ac = a < nc ? a : a0;
+            v[u] = scale * (CR ? row_dot_c(ac, rs, ia, ib, rc, U) : row_dot(ac, cap, ia, ib, n, ta, tb, U));
         }
 #pragma unroll
         for (int u = 0; u < GATHER_ILP; ++u) {
@@ -546,9 +592,15 @@ int op_gather_apply(relcp_ctx *ctx, const relcp_constraints *cs, const double *U
                     int norm2) {
     const int64_t nc = cs->count;
     if (nc == 0) return RELCP_OK;
-    int grid = grid_for(nc, RELCP_NT, 4);
-    k_gather<<<grid, RELCP_NT, 0, ctx->stream>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, U, scale, y,
-                                                 norm2, ctx->partials.p, ctx->counter.p, ctx->st.p);
+    const int grid = grid_for(nc, RELCP_NT, ctx->op_compact ? GATHER_MINB_CR : 4);
+    if (ctx->op_compact)
+        k_gather<true><<<grid, RELCP_NT, 0, ctx->stream>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb,
+                                                           ctx->op_rs, ctx->rc.p, U, scale, y, norm2, ctx->partials.p,
+                                                           ctx->counter.p, ctx->st.p);
+    else
+        k_gather<false><<<grid, RELCP_NT, 0, ctx->stream>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb,
+                                                            ctx->op_rs, ctx->rc.p, U, scale, y, norm2, ctx->partials.p,
+                                                            ctx->counter.p, ctx->st.p);
     CKL();
     return RELCP_OK;
 }
