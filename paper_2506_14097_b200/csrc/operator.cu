@@ -35,6 +35,9 @@
 #ifndef K6_REVERSE
 #define K6_REVERSE 1
 #endif
+#ifndef SCATTER_WAVES
+#define SCATTER_WAVES 8  // grid cap = 148 * SCATTER_MINB * waves (grid-stride over 32-body groups)
+#endif
 #ifndef SCATTER_MINB
 #define SCATTER_MINB 8   // resident blocks per SM the register budget must allow (64 regs at 4 warps)
 #endif
@@ -391,7 +394,8 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
     const int64_t E = ctx->op_sorted ? ctx->op_nc : 2 * ctx->op_nc;
     const int64_t nwarp = (nb + 31) / 32;
     int64_t grid = (nwarp + SCATTER_WPB - 1) / SCATTER_WPB;
-    if (grid > (int64_t)RELCP_SM_COUNT * 64) grid = (int64_t)RELCP_SM_COUNT * 64;
+    if (grid > (int64_t)RELCP_SM_COUNT * SCATTER_MINB * SCATTER_WAVES)
+        grid = (int64_t)RELCP_SM_COUNT * SCATTER_MINB * SCATTER_WAVES;
     if (grid < 1) grid = 1;
     const unsigned G = (unsigned)grid, T = 32 * SCATTER_WPB;
     const int *pa = ctx->pa.p;

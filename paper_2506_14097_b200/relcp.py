@@ -147,6 +147,23 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
 
+def _dptr(t, dtype, numel: int, name: str, optional: bool = False):
+    """Device pointer of a tensor handed to the library: CUDA, `dtype`,
+    contiguous, at least `numel` elements.  Anything else raises ValueError
+    here (a host, strided or short buffer would fault inside a kernel)."""
+    if t is None:
+        if optional:
+            return None
+        raise ValueError(f"{name}: required")
+    ok = (torch.is_tensor(t) and t.is_cuda and t.dtype == dtype and t.is_contiguous()
+          and t.numel() >= numel)
+    if not ok:
+        desc = (f"{t.dtype} on {t.device}, contiguous={t.is_contiguous()}, numel={t.numel()}"
+                if torch.is_tensor(t) else type(t).__name__)
+        raise ValueError(f"{name}: need a contiguous CUDA {dtype} tensor with >= {numel} elements, got {desc}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
 class BodyState:
     """Device-resident SoA body arrays (fp64; kinematic int32)."""
 
@@ -169,8 +186,11 @@ class BodyState:
                    sc.get("kinematic"), device=device, shape=sc.get("shape"))
 
     def view(self) -> Bodies:
-        return Bodies(self.n, _ptr(self.pos), _ptr(self.quat), _ptr(self.axes), _ptr(self.vel), _ptr(self.inv_mass),
-                      _ptr(self.inv_inertia), _ptr(self.kinematic), _ptr(self.shape))
+        n, f, i = self.n, torch.float64, torch.int32
+        return Bodies(n, _dptr(self.pos, f, 3 * n, "pos"), _dptr(self.quat, f, 4 * n, "quat"),
+                      _dptr(self.axes, f, 3 * n, "axes"), _dptr(self.vel, f, 6 * n, "vel", True),
+                      _dptr(self.inv_mass, f, n, "inv_mass", True), _dptr(self.inv_inertia, f, 3 * n, "inv_inertia", True),
+                      _dptr(self.kinematic, i, n, "kinematic", True), _dptr(self.shape, i, n, "shape", True))
 
 
 class ConstraintStore:
@@ -205,8 +225,11 @@ class ConstraintStore:
         return cs
 
     def view(self) -> Constraints:
-        v = Constraints(self.capacity, self.count, _ptr(self.ia), _ptr(self.ib), _ptr(self.gen), _ptr(self.n),
-                        _ptr(self.ta), _ptr(self.tb), _ptr(self.phi), _ptr(self.q), _ptr(self.lam), _ptr(self.g))
+        c, f, i = self.capacity, torch.float64, torch.int32
+        v = Constraints(c, self.count, _dptr(self.ia, i, c, "ia"), _dptr(self.ib, i, c, "ib"),
+                        _dptr(self.gen, i, c, "gen"), _dptr(self.n, f, 3 * c, "n"), _dptr(self.ta, f, 3 * c, "ta"),
+                        _dptr(self.tb, f, 3 * c, "tb"), _dptr(self.phi, f, c, "phi"), _dptr(self.q, f, c, "q"),
+                        _dptr(self.lam, f, c, "lambda"), _dptr(self.g, f, c, "g"))
         self._view = v
         return v
 
@@ -281,8 +304,11 @@ class Context:
         phi_t = torch.as_tensor(np.asarray(phi) if not torch.is_tensor(phi) else phi, dtype=torch.float64,
                                 device=dev).contiguous()
         bv, cv = bodies.view(), cs.view()
-        rc = self.L.relcp_load_constraints(self.h, ctypes.byref(bv), ctypes.byref(cv), ia_t.numel(), _ptr(ia_t),
-                                           _ptr(ib_t), _ptr(n_t), _ptr(ra_t), _ptr(rb_t), _ptr(phi_t))
+        m, f = ia_t.numel(), torch.float64
+        rc = self.L.relcp_load_constraints(self.h, ctypes.byref(bv), ctypes.byref(cv), m,
+                                           _dptr(ia_t, torch.int32, m, "ia"), _dptr(ib_t, torch.int32, m, "ib"),
+                                           _dptr(n_t, f, 3 * m, "n"), _dptr(ra_t, f, 3 * m, "ra"),
+                                           _dptr(rb_t, f, 3 * m, "rb"), _dptr(phi_t, f, m, "phi"))
         cs.sync_from(cv)
         self._check(rc)
 
@@ -294,12 +320,16 @@ class Context:
     def delassus_apply(self, bodies: BodyState, cs: ConstraintStore, x: torch.Tensor, y: torch.Tensor,
                        scale: float = 1.0):
         bv, cv = bodies.view(), cs.view()
-        self._check(self.L.relcp_delassus_apply(self.h, ctypes.byref(bv), ctypes.byref(cv), _ptr(x), _ptr(y),
+        m = cs.count
+        self._check(self.L.relcp_delassus_apply(self.h, ctypes.byref(bv), ctypes.byref(cv),
+                                                _dptr(x, torch.float64, m, "x"), _dptr(y, torch.float64, m, "y"),
                                                 float(scale)))
 
     def wrench(self, bodies: BodyState, cs: ConstraintStore, x: torch.Tensor, F=None, U=None):
         bv, cv = bodies.view(), cs.view()
-        self._check(self.L.relcp_wrench(self.h, ctypes.byref(bv), ctypes.byref(cv), _ptr(x), _ptr(F), _ptr(U)))
+        f, m, n = torch.float64, cs.count, bodies.n
+        self._check(self.L.relcp_wrench(self.h, ctypes.byref(bv), ctypes.byref(cv), _dptr(x, f, m, "x"),
+                                        _dptr(F, f, 6 * n, "F", True), _dptr(U, f, 6 * n, "U", True)))
 
     def solve_lcp(self, bodies: BodyState, cs: ConstraintStore):
         bv, cv = bodies.view(), cs.view()
@@ -322,7 +352,8 @@ class Context:
     def step(self, bodies: BodyState, cs: ConstraintStore, f_ext: torch.Tensor | None = None):
         bv, cv = bodies.view(), cs.view()
         rep = StepReport()
-        rc = self.L.relcp_step(self.h, ctypes.byref(bv), _ptr(f_ext), ctypes.byref(cv), ctypes.byref(rep))
+        fe = _dptr(f_ext, torch.float64, 6 * bodies.n, "f_ext", True)
+        rc = self.L.relcp_step(self.h, ctypes.byref(bv), fe, ctypes.byref(cv), ctypes.byref(rep))
         cs.sync_from(cv)
         self._check(rc)
         d = rep.as_dict()
@@ -352,8 +383,11 @@ class Context:
         return pi[:m], pj[:m]
 
     def snsd_pairs(self, bodies: BodyState, pi, pj):
-        pi = torch.as_tensor(np.asarray(pi), dtype=torch.int32, device="cuda") if not torch.is_tensor(pi) else pi
-        pj = torch.as_tensor(np.asarray(pj), dtype=torch.int32, device="cuda") if not torch.is_tensor(pj) else pj
+        def idx(a):
+            if torch.is_tensor(a):
+                return a.to(device="cuda", dtype=torch.int32).contiguous()
+            return torch.as_tensor(np.asarray(a), dtype=torch.int32, device="cuda")
+        pi, pj = idx(pi), idx(pj)
         m = pi.numel()
         phi = torch.empty(max(m, 1), dtype=torch.float64, device="cuda")
         nrm = torch.empty(3, max(m, 1), dtype=torch.float64, device="cuda")
@@ -361,7 +395,10 @@ class Context:
         rb = torch.empty_like(nrm)
         st = torch.empty(max(m, 1), dtype=torch.int32, device="cuda")
         bv = bodies.view()
-        self._check(self.L.relcp_snsd_pairs(self.h, ctypes.byref(bv), m, _ptr(pi), _ptr(pj), _ptr(phi), _ptr(nrm),
-                                            _ptr(ra), _ptr(rb), _ptr(st)))
+        if pj.numel() != m:
+            raise ValueError("snsd_pairs: pi and pj differ in length")
+        self._check(self.L.relcp_snsd_pairs(self.h, ctypes.byref(bv), m, _dptr(pi, torch.int32, m, "pi"),
+                                            _dptr(pj, torch.int32, m, "pj"), _ptr(phi), _ptr(nrm), _ptr(ra), _ptr(rb),
+                                            _ptr(st)))
         torch.cuda.synchronize()
         return phi[:m], nrm[:, :m], ra[:, :m], rb[:, :m], st[:m]

@@ -49,3 +49,25 @@ def test_default_params_and_no_gpu_refusal():
         relcp.Context()
     bad = relcp.default_params(dt=-1.0)
     assert L.relcp_create(ctypes.byref(h), ctypes.byref(bad), None) == relcp.E_ARG
+
+
+def test_binding_refuses_bad_buffers():
+    """The binding validates every tensor it hands to the C ABI: host, wrong
+    dtype, strided or short buffers raise ValueError before any kernel can
+    dereference them; optional arguments may be None."""
+    import torch
+    from paper_2506_14097_b200 import relcp as R
+    f = torch.float64
+    assert R._dptr(None, f, 3, "vel", optional=True) is None
+    with pytest.raises(ValueError, match="required"):
+        R._dptr(None, f, 3, "pos")
+    with pytest.raises(ValueError, match="CUDA"):
+        R._dptr(torch.zeros(8, dtype=f), f, 3, "pos")  # host tensor
+    with pytest.raises(ValueError):
+        R._dptr(torch.zeros(8, dtype=torch.float32), f, 3, "pos")
+    with pytest.raises(ValueError):
+        R._dptr(torch.zeros(4, 4, dtype=f).T, f, 3, "pos")
+    with pytest.raises(ValueError):
+        R._dptr(torch.zeros(2, dtype=f), f, 3, "pos")
+    with pytest.raises(ValueError):
+        R._dptr([0.0, 1.0, 2.0], f, 3, "pos")
