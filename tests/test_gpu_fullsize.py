@@ -101,7 +101,7 @@ def test_fullsize_cfg5_generate(orc, R, cfg5_full):
             assert ((int(a), int(b2)) in rows) == (f < sc["cutoff"])
 
 
-def test_fullsize_cfg5_step_invariants(R, cfg5_full):
+def test_fullsize_cfg5_step_invariants(orc, R, cfg5_full):
     """The bench workload (2 recursions, 3000-iteration LCP cap)."""
     sc = cfg5_full
     ctx = _ctx(R, sc, lcp_tol=1e-8, lcp_max_iter=3000, max_recursions=2)
@@ -130,6 +130,33 @@ def test_fullsize_cfg5_step_invariants(R, cfg5_full):
     dP = ((bodies.vel[:, :3] - v0) * mass[:, None]).sum(0)
     scale = ((bodies.vel[:, :3] - v0).abs() * mass[:, None]).sum()
     assert float(dP.abs().max()) <= 1e-12 * float(scale)
+    # the last LCP's g on the final (augmented) store is the oracle's
+    # s D^T W D lambda + q with W frozen at C^k (the generator's orientations)
+    c = cs.to_numpy()
+    Alam = orc.delassus_apply(orc.body_W(sc), c["ia"], c["ib"], c["n"], c["ta"], c["tb"], sc["dt"] ** 2, c["lam"])
+    assert len(c["ia"]) == rep["n_c"][-1]
+    assert np.max(np.abs(c["g"] - (Alam + c["q"]))) <= 1e-12 * np.max(np.abs(Alam))
+
+
+def test_fullsize_cfg5_solve_against_oracle_operator(orc, R, cfg5_full):
+    """cfg5 A_0 (5.3M rows) solved in the bench's launch configuration (BB,
+    3000-iteration cap, compact-row K7): the g the GPU returns equals the
+    oracle's own s D^T W D lambda + q on EVERY row (1e-12 of the scale of
+    A lambda), and the returned pair satisfies lambda >= 0 and the reported
+    residual r = max |min(lambda, g)|."""
+    sc = cfg5_full
+    ctx = _ctx(R, sc, lcp_tol=1e-8, lcp_max_iter=3000)
+    bodies = R.BodyState.from_scene(sc)
+    cs = R.ConstraintStore(12 * sc["n"])
+    ctx.generate_contacts(bodies, cs)
+    rep = ctx.solve_lcp(bodies, cs)
+    c = cs.to_numpy()
+    lam, g, q = c["lam"], c["g"], c["q"]
+    assert np.all(lam >= 0)
+    assert abs(np.max(np.abs(np.minimum(lam, g))) - rep["residual"]) <= 1e-15 + 1e-12 * rep["residual"]
+    W = orc.body_W(sc)
+    Alam = orc.delassus_apply(W, c["ia"], c["ib"], c["n"], c["ta"], c["tb"], sc["dt"] ** 2, lam)
+    assert np.max(np.abs(g - (Alam + q))) <= 1e-12 * np.max(np.abs(Alam))
 
 
 def test_fullsize_cfg4_lcp(R):
