@@ -11,7 +11,9 @@ Plain, slow, obviously correct:
      are written out below in numpy, line by line, in the paper's
     own order and notation (Phi-tilde, D_n, b_n = A_n iota(x_{n-1}) - g~_{n-1},
     incremental trial configurations C_{n+1} = C_n + dt G M D_n (g_n - iota g_{n-1})).
-  * `enumerate_lcp` solves tiny dense LCPs by trying every support (brute force).
+  * `enumerate_lcp` solves tiny dense LCPs by trying every support (brute force);
+    `pgs` (projected Gauss-Seidel on the assembled A, plain C) cross-checks
+    the BB solutions with a different algorithm.
 
 Citations: P:Lnnn = /root/reference/PAPER.md line; R<k> = reading k in DESIGN.md.
 Parity pins: tests/test_oracle_*.py.  Whole-step trajectories of the BASELINE
@@ -65,6 +67,8 @@ def lib():
         L.orc_bbpgd.restype = None
         L.orc_bbpgd.argtypes = [i64, i64, P, P, P, P, P, P, ctypes.c_double, P, P, P,
                                 ctypes.c_double, i64, ctypes.c_int, P]
+        L.orc_pgs_csr.restype = None
+        L.orc_pgs_csr.argtypes = [i64, P, P, P, P, P, P, ctypes.c_double, i64, P]
         _lib = L
     return _lib
 
@@ -229,6 +233,42 @@ def bbpgd(W, ia, ib, nrm, ta, tb, s, q, x0=None, tol=1e-10, max_iter=1_000_000, 
                     _p(g), float(tol), int(max_iter), int(power_iters), _p(info))
     return x, g, dict(iterations=int(info[0]), residual=float(info[1]), converged=bool(info[2]),
                       L=float(info[3]))
+
+
+def assemble_A(W, ia, ib, nrm, ta, tb, s):
+    """A = s D^T W D as a scipy CSR matrix, from the plain definition: column
+    alpha of D is -[n; t_a] on body ia and +[n; t_b] on body ib (P:L154-157,
+    P:L1413), W block diagonal (N 6x6 blocks), A_n = s D^T W D."""
+    import scipy.sparse as sp
+    nb, nc = W.shape[0], len(ia)
+    rows = np.concatenate([6 * np.asarray(ia)[:, None] + np.arange(6), 6 * np.asarray(ib)[:, None] + np.arange(6)])
+    vals = np.concatenate([-np.hstack([nrm, ta]), np.hstack([nrm, tb])])
+    cols = np.concatenate([np.repeat(np.arange(nc), 6).reshape(nc, 6)] * 2)
+    D = sp.csr_matrix((vals.ravel(), (rows.ravel(), cols.ravel())), shape=(6 * nb, nc))
+    blk = np.asarray(W, dtype=np.float64).reshape(nb, 6, 6)
+    r_ = (6 * np.arange(nb)[:, None, None] + np.arange(6)[None, :, None]) + 0 * np.arange(6)[None, None, :]
+    c_ = (6 * np.arange(nb)[:, None, None] + np.arange(6)[None, None, :]) + 0 * np.arange(6)[None, :, None]
+    Wb = sp.csr_matrix((blk.ravel(), (r_.ravel(), c_.ravel())), shape=(6 * nb, 6 * nb))  # block diagonal
+    return (s * (D.T @ Wb @ D)).tocsr()
+
+
+def pgs(A, q, x0=None, tol=1e-12, max_sweeps=200_000):
+    """Projected Gauss-Seidel on the assembled A (CSR) --
+    an LCP algorithm independent of bbpgd.  Returns x, g, info dict."""
+    import scipy.sparse as sp
+    A = sp.csr_matrix(A)
+    A.sort_indices()
+    n = A.shape[0]
+    indptr = _c(A.indptr, np.int64)
+    indices = _c(A.indices, np.int32)
+    data = _c(A.data, np.float64)
+    q = _c(q, np.float64)
+    x = np.zeros(n) if x0 is None else _c(x0, np.float64).copy()
+    g = np.empty(n)
+    info = np.zeros(3)
+    lib().orc_pgs_csr(n, _p(indptr), _p(indices), _p(data), _p(q), _p(x), _p(g), float(tol), int(max_sweeps),
+                      _p(info))
+    return x, g, dict(sweeps=int(info[0]), residual=float(info[1]), converged=bool(info[2]))
 
 
 def enumerate_lcp(A, q, tol=1e-12, all_solutions=False):

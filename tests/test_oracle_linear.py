@@ -199,3 +199,52 @@ def test_lemma5_unique_D_x(orc):
     F2, _ = orc.wrench(W, ia, ib, n, ta, tb, x2)
     assert np.abs(F1 - F2).max() <= 1e-6 * np.abs(F1).max()
     assert np.abs(x1 - x2).max() > 1e-3 * np.abs(x1).max()   # multipliers differ
+
+
+def test_assembled_A_equals_matrix_free(orc):
+    """The explicitly assembled s D^T W D (scipy, from the column definition
+    of D) equals the matrix-free apply on random vectors."""
+    b, ia, ib, n, ta, tb, W = _net(orc, 60, 200, 21)
+    s = 3e-3
+    A = orc.assemble_A(W, ia, ib, n, ta, tb, s)
+    rng = np.random.default_rng(2)
+    for _ in range(3):
+        x = rng.standard_normal(200)
+        y = orc.delassus_apply(W, ia, ib, n, ta, tb, s, x)
+        assert np.abs(A @ x - y).max() <= 1e-13 * np.abs(y).max()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_pgs_vs_enumeration(orc, seed):
+    """PGS (a different algorithm on the assembled matrix) reaches the
+    brute-force enumeration's solution on tiny contact LCPs."""
+    b, ia, ib, n, ta, tb, W = _net(orc, 6, 8 + seed % 3, 40 + seed)
+    s = 1e-2
+    A = orc.assemble_A(W, ia, ib, n, ta, tb, s)
+    q = np.random.default_rng(seed).uniform(-1, 1, len(ia))
+    x, g, info = orc.pgs(A, q, tol=1e-13)
+    ref = orc.enumerate_lcp(A.toarray(), q)
+    assert info["converged"]
+    Ad = A.toarray()
+    assert np.abs(Ad @ x - Ad @ ref).max() <= 1e-9 * (1 + np.abs(q).max())
+    if np.linalg.eigvalsh(Ad).min() > 1e-8 * np.abs(Ad).max():
+        np.testing.assert_allclose(x, ref, atol=1e-8 * (1 + np.abs(ref).max()))
+
+
+def test_bbpgd_vs_pgs_cfg1(orc):
+    """The oracle's BB solution of cfg1's A_0 LCP (435 rows, overlapping
+    start) equals projected Gauss-Seidel's on the assembled matrix: D lambda
+    and g agree (unique by Lemma 5), and lambda too."""
+    sc = scenes.cfg1()
+    r = orc.relcp_step(sc, snsd_only=True, lcp_tol=1e-12)
+    c, W, s = r["constraints"], r["W"], r["s"]
+    q = r["q_hist"][0]
+    A = orc.assemble_A(W, c["ia"], c["ib"], c["n"], c["ta"], c["tb"], s)
+    x_p, g_p, info = orc.pgs(A, q, tol=1e-12)
+    assert info["converged"]
+    x_b, g_b = c["lam"], r["g_hist"][0]
+    F_p, _ = orc.wrench(W, c["ia"], c["ib"], c["n"], c["ta"], c["tb"], x_p)
+    F_b, _ = orc.wrench(W, c["ia"], c["ib"], c["n"], c["ta"], c["tb"], x_b)
+    assert np.abs(F_p - F_b).max() <= 1e-6 * np.abs(F_b).max()
+    assert np.abs(g_p - g_b).max() <= 1e-6 * np.abs(q).max()
+    assert np.abs(x_p - x_b).max() <= 1e-6 * np.abs(x_b).max()
