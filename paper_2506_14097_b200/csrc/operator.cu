@@ -19,8 +19,10 @@
 //     through a shared-memory transpose (coalesced).  The kernel is bound by
 //     the L1 data pipe (staging + bank-conflicted per-lane sums + the b-side
 //     x / g gathers); see profiles/README.md.
-//   * gather y = s D^T U (K7) is a constraint-major streaming pass over the
-//     SoA store (coalesced n / t_a / t_b planes) with U_a, U_b read from L2.
+//   * gather y = s D^T U (K7, k_gather) is a constraint-major streaming pass
+//     with U_a, U_b read from L2.  When every row has t . n ~ 0 (t = r x n),
+//     the row passes read a compact copy of the rows built here (k_compact,
+//     rows.cuh: 6 instead of 9 fp64 per row); otherwise the store's planes.
 //   * k_fused_rows: the fused-APGD row pass (lcp.cu solver 2).
 #include "common.cuh"
 #include "reduce.cuh"
