@@ -22,7 +22,10 @@
 #define ITER_MINB 4  // resident K7 blocks per SM (register budget); grid = 148 * ITER_MINB
 #endif
 #ifndef ITER_MINB_CR
-#define ITER_MINB_CR 3  // with compact rows (decode registers): same-box A/B 113 us vs 124 us at 4 with spills
+#define ITER_MINB_CR 2  // with compact rows (decode registers, 128 per thread): same-box A/B
+#endif                  // ILP 4 x 2 blocks 0.273 ms per iteration, ILP 2 x 3 blocks 0.276, ILP 1 x 4 0.283
+#ifndef ITER_ILP_CR
+#define ITER_ILP_CR 4
 #endif
 #ifndef ITER_ILP
 #define ITER_ILP 2   // rows per thread per trip in K7
@@ -108,11 +111,12 @@ __global__ void __launch_bounds__(RELCP_NT, CR ? ITER_MINB_CR : ITER_MINB) k_lcp
     const double alpha = st->alpha;
     double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    // ITER_ILP constraints per thread per trip: independent loads in flight (ILP)
-    for (int64_t a0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a0 < nc; a0 += ITER_ILP * stride) {
-        double xo[ITER_ILP], go[ITER_ILP], qv[ITER_ILP], rd[ITER_ILP];
+    // ILP constraints per thread per trip: independent loads in flight
+    constexpr int ILP = CR ? ITER_ILP_CR : ITER_ILP;
+    for (int64_t a0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a0 < nc; a0 += ILP * stride) {
+        double xo[ILP], go[ILP], qv[ILP], rd[ILP];
 #pragma unroll
-        for (int u = 0; u < ITER_ILP; ++u) {
+        for (int u = 0; u < ILP; ++u) {
             const int64_t a = a0 + u * stride;
             const bool ok = a < nc;
             const int64_t ac = ok ? a : a0;
@@ -122,7 +126,7 @@ __global__ void __launch_bounds__(RELCP_NT, CR ? ITER_MINB_CR : ITER_MINB) k_lcp
             rd[u] = ROW_DOT(ac);
         }
 #pragma unroll
-        for (int u = 0; u < ITER_ILP; ++u) {
+        for (int u = 0; u < ILP; ++u) {
             const int64_t a = a0 + u * stride;
             if (a >= nc) continue;
             const double xn = fmax(0.0, xo[u] - alpha * go[u]);
