@@ -227,6 +227,11 @@ __device__ __forceinline__ bool better(double f, const double *n, double fb, con
     return n[2] < nb[2];
 }
 
+#ifndef SNSD_MINB
+#define SNSD_MINB 4  // resident blocks per SM for the Newton / multistart stages: 128 registers (some spills)
+                     // beats 146-168 at 1-2 blocks: SNSD 66 -> 56.5 ms per cfg5 step (same-box A/B)
+#endif
+
 // SNSD status codes (k_snsd_* outputs)
 #define SNSD_OK 0
 #define SNSD_DEGENERATE 1  // coincident centres (R4)
@@ -565,7 +570,7 @@ __global__ void __launch_bounds__(128) k_snsd_stage0(int64_t np, const int *__re
 
 // Stage 1 over the Newton list (ellipsoid pairs under the bound): Newton from
 // d/|d|; pairs needing the multistart are listed for stage 2.
-__global__ void __launch_bounds__(128) k_snsd_stage1(const int *__restrict__ nlist, const unsigned *__restrict__ n_nlist,
+__global__ void __launch_bounds__(128, SNSD_MINB) k_snsd_stage1(const int *__restrict__ nlist, const unsigned *__restrict__ n_nlist,
                                                      const int *__restrict__ pi, const int *__restrict__ pj,
                                                      const double *__restrict__ pos, const double *__restrict__ Sig,
                                                      Box3 box, double *__restrict__ phi, double *__restrict__ nrm,
@@ -589,7 +594,7 @@ __global__ void __launch_bounds__(128) k_snsd_stage1(const int *__restrict__ nli
 }
 
 // Stage 2 over the listed (overlapping / touching) pairs: uniform work per thread.
-__global__ void __launch_bounds__(128) k_snsd_stage2(const int *__restrict__ multi, const unsigned *__restrict__ n_multi,
+__global__ void __launch_bounds__(128, SNSD_MINB) k_snsd_stage2(const int *__restrict__ multi, const unsigned *__restrict__ n_multi,
                                                      const int *__restrict__ pi, const int *__restrict__ pj,
                                                      const double *__restrict__ pos, const double *__restrict__ Sig,
                                                      Box3 box, int n_dirs, const double *__restrict__ dirs,
