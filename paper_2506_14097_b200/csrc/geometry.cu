@@ -513,6 +513,9 @@ __device__ __forceinline__ void list_push(bool push, int64_t k, int *list, unsig
 // ellipsoid pairs get the lower bound Phi >= F(d/|d|) (snsd_stage1) and, when
 // it does not reject them, go to the Newton list, so that the Newton stage
 // runs with full warps (most pairs of a check are rejected by the bound).
+// SHAPES: the bodies carry a shape array (rods / tori possible); without it
+// every pair is an ellipsoid pair and the rod / torus code is compiled out.
+template <bool SHAPES>
 __global__ void __launch_bounds__(128) k_snsd_stage0(int64_t np, const int *__restrict__ pi,
                                                      const int *__restrict__ pj, const double *__restrict__ pos,
                                                      const double *__restrict__ Sig, Box3 box, double reject_above,
@@ -528,17 +531,17 @@ __global__ void __launch_bounds__(128) k_snsd_stage0(int64_t np, const int *__re
         double f, n[3], r1[3], r2[3];
         int st = -1;  // >= 0: outputs final here; -1: bound (phi only) or Newton list
         bool newton = false;
-        const int sha = shape ? shape[pi[k]] : 0, shb = shape ? shape[pj[k]] : 0;
-        if (sha == RELCP_SHAPE_SPHEROCYLINDER && shb == RELCP_SHAPE_SPHEROCYLINDER) {
+        const int sha = SHAPES ? shape[pi[k]] : 0, shb = SHAPES ? shape[pj[k]] : 0;
+        if (SHAPES && sha == RELCP_SHAPE_SPHEROCYLINDER && shb == RELCP_SHAPE_SPHEROCYLINDER) {
             const double ga[6] = {Sa.xx, Sa.xy, Sa.xz, Sa.yy, Sa.yz, Sa.zz};
             const double gb[6] = {Sb.xx, Sb.xy, Sb.xz, Sb.yy, Sb.yz, Sb.zz};
             st = rod_pair(d, ga, gb, f, n, r1, r2);
-        } else if (sha == RELCP_SHAPE_TORUS && shb == RELCP_SHAPE_TORUS) {
+        } else if (SHAPES && sha == RELCP_SHAPE_TORUS && shb == RELCP_SHAPE_TORUS) {
             const double ga[6] = {Sa.xx, Sa.xy, Sa.xz, Sa.yy, Sa.yz, Sa.zz};
             const double gb[6] = {Sb.xx, Sb.xy, Sb.xz, Sb.yy, Sb.yz, Sb.zz};
             const int64_t a = pi[k], b = pj[k];
             st = torus_pair(d, ga, gb, axes[3 * a], axes[3 * a + 1], axes[3 * b], axes[3 * b + 1], f, n, r1, r2);
-        } else if (sha != shb) {  // mixed ellipsoid-rod pairs are not defined (include/relcp.h)
+        } else if (SHAPES && sha != shb) {  // mixed ellipsoid-rod pairs are not defined (include/relcp.h)
             f = nan("");
             for (int c = 0; c < 3; ++c) n[c] = r1[c] = r2[c] = nan("");
             st = SNSD_DEGENERATE;
@@ -636,9 +639,14 @@ int geo_snsd(relcp_ctx *ctx, int64_t np, const int *pi, const int *pj, const dou
     CK(cudaMemsetAsync(ctx->counter.p + 1, 0, 2 * sizeof(unsigned), ctx->stream));
     int64_t g = (np + 127) / 128;
     if (g > 148 * 64) g = 148 * 64;
-    k_snsd_stage0<<<(unsigned)g, 128, 0, ctx->stream>>>(np, pi, pj, pos, Sig, bx, reject_above, phi, nrm, ra, rb,
-                                                        status, planes, ctx->nlist.p, ctx->counter.p + 2, shape,
-                                                        axes);
+    if (shape)
+        k_snsd_stage0<true><<<(unsigned)g, 128, 0, ctx->stream>>>(np, pi, pj, pos, Sig, bx, reject_above, phi, nrm, ra,
+                                                                  rb, status, planes, ctx->nlist.p, ctx->counter.p + 2,
+                                                                  shape, axes);
+    else
+        k_snsd_stage0<false><<<(unsigned)g, 128, 0, ctx->stream>>>(np, pi, pj, pos, Sig, bx, reject_above, phi, nrm,
+                                                                   ra, rb, status, planes, ctx->nlist.p,
+                                                                   ctx->counter.p + 2, shape, axes);
     CKL();
     k_snsd_stage1<<<148 * 8, 128, 0, ctx->stream>>>(ctx->nlist.p, ctx->counter.p + 2, pi, pj, pos, Sig, bx, phi, nrm,
                                                     ra, rb, status, planes, ctx->multi.p, ctx->counter.p + 1);
