@@ -332,6 +332,12 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
     int pending = 0, batches = 0;
     bool capturing = false, graph_timed = false;
     cudaGraphExec_t gexec = nullptr;
+    struct GraphGuard {  // destroys the replayed batch graph on every exit path
+        cudaGraphExec_t &g;
+        ~GraphGuard() {
+            if (g) cudaGraphExecDestroy(g);
+        }
+    } graph_guard{gexec};
     // `batch` BB iterations: K6 (scatter + projection) then K7 (gather + update)
     auto enqueue_batch = [&]() -> int {
         for (int j = 0; j < batch; ++j) {
@@ -422,7 +428,11 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
         pending = batch;
     }
     PHASE(ctx, "solve.loop");
-    if (gexec) CK(cudaGraphExecDestroy(gexec));
+    if (gexec) {
+        const cudaError_t e = cudaGraphExecDestroy(gexec);
+        gexec = nullptr;
+        CK(e);
+    }
     if (apgd && ctx->st_host->par) {  // the current APGD iterate lives in the second buffer
         CK(cudaMemcpyAsync(cs->lambda, xB, sizeof(double) * nc, cudaMemcpyDeviceToDevice, st));
         CK(cudaMemcpyAsync(cs->g, gB, sizeof(double) * nc, cudaMemcpyDeviceToDevice, st));
