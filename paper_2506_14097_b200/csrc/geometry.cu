@@ -9,13 +9,19 @@
 //     y_a = x_a + Sigma_a n / h_a,  y_b = x_b - Sigma_b n / h_b.
 // At a stationary point y_b - y_a = Phi n.
 //
-// GPU strategy (differs from the oracle's fixed multistart):
-//   F is concave and positively homogeneous on R^3, so a local maximum on the
-//   sphere with F > 0 is the global one.  Each thread first runs damped
-//   Riemannian Newton from d/|d|; only if that ends with F <= 0 (overlap or
-//   touching) does it sample `n_dirs` Fibonacci directions and restart Newton
-//   from the best four, keeping the largest maximum (ties: larger n.d/|d|,
-//   then lexicographically smaller n; R4).
+// GPU strategy (differs from the oracle's fixed multistart), three kernels
+// over compacted work lists so that every stage runs with full warps:
+//   stage 0  every pair: F is concave and positively homogeneous on R^3, so
+//            Phi >= F(d/|d|); a pair whose bound already clears the threshold
+//            is final (status BOUND, phi = the bound); rods and tori are
+//            solved here in full; the rest is listed (one atomic per warp).
+//   stage 1  listed pairs: damped Riemannian Newton from d/|d|; a maximum with
+//            F > 0 is the global one (concavity); F <= 0 (overlap or touching)
+//            goes to the stage-2 list with the Newton result as incumbent.
+//   stage 2  listed pairs: sample the `n_dirs` Fibonacci directions (table
+//            built once per context, k_dirs), Newton from the best four, keep
+//            the largest maximum (ties: larger n.d/|d|, then lexicographically
+//            smaller n; R4).
 #include "common.cuh"
 #include "reduce.cuh"
 
