@@ -396,6 +396,24 @@ def test_step_parity_cfg1_relaxed(orc, R):
     assert rep["recursions"] == 0 and rep["max_overlap"] <= 1e-5
 
 
+def test_reduction_corollary_gpu(orc, R):
+    """P:L895-900 on the GPU: from the overlap-free cfg1 state, dt = 1e-3 and
+    1e-4 end after the recursion-0 solve, the overlap left (eta_1) matches the
+    oracle's and falls ~dt^2."""
+    eta = {}
+    for dt in (1e-3, 1e-4):
+        sc = scenes.cfg1_relaxed(dt=dt)
+        r = orc.relcp_step(sc, lcp_tol=1e-12)
+        ctx = _ctx(R, sc, lcp_tol=1e-12, lcp_max_iter=2_000_000)
+        bodies = R.BodyState.from_scene(sc)
+        cs = R.ConstraintStore(8000)
+        rep = ctx.step(bodies, cs)
+        assert rep["recursions"] == 0 == r["recursions"]
+        assert abs(rep["max_overlap"] - r["max_overlap"]) <= 1e-9
+        eta[dt] = rep["max_overlap"]
+    assert eta[1e-4] < eta[1e-3] / 30.0
+
+
 def test_step_parity_cfg1_bigdt(orc, R):
     """cfg1-bigdt: the relaxed start at dt = 0.1 augments several times; the
     appended rows, generations and the accepted state match the oracle."""
