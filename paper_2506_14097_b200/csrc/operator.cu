@@ -16,9 +16,10 @@
 //     streamed in coalesced 64-entry tiles into shared memory and each lane
 //     sums its own body's entries in order (fixed association: bitwise
 //     deterministic, no atomics), then applies W_b (SoA planes) and stores U_b
-//     through a shared-memory transpose (coalesced).  The kernel is bound by
-//     the L1 data pipe (staging + bank-conflicted per-lane sums + the b-side
-//     x / g gathers); see profiles/README.md.
+//     through a shared-memory transpose (coalesced).  The kernel reaches 78 %
+//     of the copy bandwidth on its bytes and is limited by load latency (the
+//     dependent chains pa -> rows, row_ptr -> ecid -> x / g gathers); see
+//     profiles/README.md for the variants measured against it.
 //   * gather y = s D^T U (K7, k_gather) is a constraint-major streaming pass
 //     with U_a, U_b read from L2.  When every row has t . n ~ 0 (t = r x n),
 //     the row passes read a compact copy of the rows built here (k_compact,
