@@ -48,8 +48,15 @@ torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 20
 print(f"N={n} N_C={nc} apply {ms:.4f} ms  alg {(176 * nc + 152 * n) / ms / 1e6:.0f} GB/s", flush=True)
 ctx.set_timing(True)
+prof = os.environ.get("KBENCH_PROFILE_SOLVE") == "1"  # ncu --profile-from-start off: only this solve
+if prof:
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
 t = time.time()
 rep = ctx.solve_lcp(bodies, cs)
+if prof:
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
 st = ctx.stats()
 it, sp = max(1, st["iter_timed"]), max(1, st["split_timed"])
 print(f"solve {rep['iterations']} it in {time.time() - t:.3f}s; scatter {st['scatter_ms'] / sp:.4f} ms "
