@@ -134,8 +134,11 @@ typedef struct relcp_bodies {
 /* Constraint store: SoA, append-only within a step (App. D1).
  *   count        host-side element count (in/out; library updates it).
  *   ia, ib, gen  (capacity) int32: body ids (ia < ib) and the recursion index
- *                that appended the row (0 = A_0).  Within a generation block
- *                rows are sorted by (ia, ib) (R18).
+ *                that appended the row (0 = A_0).  Rows the library writes
+ *                (generate, check/augment, step) keep the whole store sorted
+ *                by (ia, ib, gen) (R18) provided the rows already present are
+ *                (ia, ib)-sorted; a store in another order is appended to
+ *                unchanged (every call accepts any row order).
  *   n, ta, tb    (3, capacity) planes: component k of row alpha at
  *                [k*capacity + alpha]; unit normal n, torque arms t_a, t_b
  *                frozen at the discovery configuration (R9).

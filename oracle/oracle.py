@@ -462,8 +462,8 @@ def relcp_step(sc, max_recursions: int = 50, lcp_tol: float = 1e-10, f_ext=None,
     U_new = U_free + sigma * Uc
     quat_out = quat_n / np.linalg.norm(quat_n, axis=1, keepdims=True)
     pos_out = pos_n.copy()
-    if np.all(box > 0):
-        pos_out = pos_out - box * np.floor(pos_out / box)
+    per = np.asarray(box) > 0                # wrap each periodic axis (box[k] > 0; min_image is per axis)
+    pos_out[:, per] = pos_out[:, per] - box[per] * np.floor(pos_out[:, per] / box[per])
     max_overlap = 0.0
     ci, cj = cand
     phin, *_ = snsd(pos_n, quat_n, axes, box, ci, cj, n_fib, shape)

@@ -102,17 +102,17 @@ __global__ void __launch_bounds__(RELCP_NT) k_trial(int64_t nb, double dt, doubl
     if (grid_reduce_last<1>(acc, ops, part, counter, sh) && threadIdx.x == 0) out[0] = sqrt(acc[0]);
 }
 
-// Accept C^{k+1} = C_{n+1}: wrap positions into the periodic box,
+// Accept C^{k+1} = C_{n+1}: wrap positions into the periodic box
+// (every axis with box[c] > 0),
 // normalise quaternions, U^{k+1} = U_tot.
 __global__ void k_accept(int64_t nb, double bx, double by, double bz, const double *__restrict__ pt,
                          const double *__restrict__ qt, const double *__restrict__ utot, double *pos, double *quat,
                          double *vel) {
     for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
         const double bxs[3] = {bx, by, bz};
-        const bool wrap = bx > 0.0 && by > 0.0 && bz > 0.0;
-        for (int c = 0; c < 3; ++c) {
+        for (int c = 0; c < 3; ++c) {  // each periodic axis separately (box[c] > 0)
             double v = pt[3 * b + c];
-            if (wrap) v -= bxs[c] * floor(v / bxs[c]);
+            if (bxs[c] > 0.0) v -= bxs[c] * floor(v / bxs[c]);
             pos[3 * b + c] = v;
         }
         double s = qt[4 * b], x = qt[4 * b + 1], y = qt[4 * b + 2], z = qt[4 * b + 3];
@@ -341,6 +341,8 @@ static int check_impl(relcp_ctx *ctx, const relcp_bodies *Ck, relcp_constraints 
     CK(cudaStreamSynchronize(ctx->stream));
     const double delta = ctx->red_host[0];
     PHASE(ctx, "chk.scatter_trial");
+    if (!isfinite(delta))
+        return set_err(ctx, RELCP_E_NAN, "check: non-finite trial displacement (velocities or multipliers)");
     // R7: widen the candidate margin until it exceeds the largest approach 2 delta
     double m = ctx->margin;
     while (m <= 2.0 * delta) m *= 2.0;

@@ -74,7 +74,17 @@ struct LcpState {
     double theta;   // APGD momentum parameter
     double beta;    // APGD extrapolation weight for the next step
     double alpha_next;  // fused BB: step of the pass after the next (one-step delay)
+    // BB nonmonotone safeguard (GLL / SPG line search, lcp.cu): the last
+    // RELCP_GLL_M objective values f(x) = 1/2 x^T (g + q), the step t along
+    // d = x+ - x of the last update and whether the current iterate is the
+    // blend x + t d of the two slots (fix = 1) rather than the full step.
+    double f_cur;
+    double fhist[10];
+    double t_ls;
+    int fix;
+    int n_ls;        // iterations whose full BB step the line search shortened
 };
+#define RELCP_GLL_M 10
 
 // Per-body mobility block W_b in a single 7-double form, stored as 7 SoA
 // planes W[k * nb + b]:

@@ -300,8 +300,12 @@ __global__ void k_dirs(int n_dirs, double *__restrict__ dirs) {
     }
 }
 
-// Stage 2 (overlap / touching): multistart from the best `n_dirs`-sample
-// directions against the incumbent (nb, status st_best) from stage 1.
+// Stage 2 (overlap / touching): multistart from `n_dirs`-sample directions in
+// distinct basins (angular non-maximum suppression, cos > SNSD_SEP_COS = same
+// basin) against the incumbent (nb, status st_best) from stage 1.
+#ifndef SNSD_SEP_COS
+#define SNSD_SEP_COS 0.9  // ~26 deg
+#endif
 __device__ int snsd_stage2(const double *d, const Sym &Sa, const Sym &Sb, int n_dirs,
                            const double *__restrict__ dirs, double *nb, int st_best, double &phi, double *nout,
                            double *ra, double *rb) {
@@ -311,7 +315,13 @@ __device__ int snsd_stage2(const double *d, const Sym &Sa, const Sym &Sb, int n_
     feval(nb, d, Sa, Sb, Eb);
     double fb = Eb.f;
     {
-        // overlap / touching: multistart from the best sampled directions
+        // overlap / touching: Newton from up to K sampled directions that lie
+        // in DIFFERENT basins.  One pass over the sample keeps K leaders with
+        // online non-maximum suppression: a direction within SNSD_SEP_COS of a
+        // leader replaces that leader if its value is larger and is dropped
+        // otherwise; a direction near no leader enters if it beats the worst.
+        // (Leaders hold sample indices; their directions are re-read from the
+        // table, which stays in L1.)  Ties keep the earlier sample.
         constexpr int K = 4;
         double topf[K];
         int topi[K];
@@ -321,16 +331,35 @@ __device__ int snsd_stage2(const double *d, const Sym &Sa, const Sym &Sb, int n_
             // warp-uniform address: one broadcast load per plane
             const double m[3] = {__ldg(dirs + i), __ldg(dirs + n_dirs + i), __ldg(dirs + 2 * n_dirs + i)};
             const double f = fval(m, d, Sa, Sb);
-            if (f > topf[K - 1]) {
-                int p = K - 1;
-                while (p > 0 && topf[p - 1] < f) {
-                    topf[p] = topf[p - 1];
-                    topi[p] = topi[p - 1];
-                    --p;
-                }
-                topf[p] = f;
-                topi[p] = i;
+            if (!(f > topf[K - 1]) && topi[K - 1] >= 0) {
+                // cannot enter; it may still only replace a nearby leader, which
+                // needs f > that leader's value >= the worst: nothing to do
+                continue;
             }
+            int near = -1;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if (near < 0 && topi[k] >= 0) {
+                    const int j = topi[k];
+                    const double c = m[0] * __ldg(dirs + j) + m[1] * __ldg(dirs + n_dirs + j) +
+                                     m[2] * __ldg(dirs + 2 * n_dirs + j);
+                    if (c > SNSD_SEP_COS) near = k;
+                }
+            }
+            int p;
+            if (near >= 0) {
+                if (!(f > topf[near])) continue;
+                p = near;  // replace the nearby leader, then restore the order
+            } else {
+                p = K - 1;  // evict the worst
+            }
+            while (p > 0 && topf[p - 1] < f) {
+                topf[p] = topf[p - 1];
+                topi[p] = topi[p - 1];
+                --p;
+            }
+            topf[p] = f;
+            topi[p] = i;
         }
         for (int k = 0; k < K; ++k) {
             if (topi[k] < 0) continue;

@@ -12,6 +12,8 @@
 //               block finalizes alpha / convergence on the device.
 // Kernels early-exit once LcpState.done is set, so the host enqueues
 // `check_every` iterations blindly and reads the state once per batch.
+#include <type_traits>
+
 #include "common.cuh"
 #include "reduce.cuh"
 
@@ -57,6 +59,11 @@ __global__ void k_state_init(LcpState *st, int64_t nc, double tol, long long max
     st->par = 0;
     st->theta = 1.0;
     st->beta = 0.0;
+    st->f_cur = 0.0;
+    for (int k = 0; k < RELCP_GLL_M; ++k) st->fhist[k] = -INFINITY;
+    st->t_ls = 1.0;
+    st->fix = 0;
+    st->n_ls = 0;
 }
 
 // g = s D^T U + q for the (projected) warm start; r_0; alpha_0 = 1/L.
@@ -69,21 +76,25 @@ __global__ void __launch_bounds__(RELCP_NT) k_lcp_init(int64_t nc, int64_t cap, 
                                                        const double *__restrict__ q, const double *__restrict__ x,
                                                        double *__restrict__ g, double *part, unsigned *counter,
                                                        LcpState *st) {
-    __shared__ double sh[64];
-    double acc[2] = {0.0, 0.0};
+    __shared__ double sh[3 * 32];
+    double acc[3] = {0.0, 0.0, 0.0};
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
-        double gv = fma(s, ROW_DOT(a), q[a]);
+        const double qa = q[a], xa = x[a];
+        double gv = fma(s, ROW_DOT(a), qa);
         g[a] = gv;
-        acc[0] = fmax(acc[0], fabs(fmin(x[a], gv)));
+        acc[0] = fmax(acc[0], fabs(fmin(xa, gv)));
         acc[1] = fmax(acc[1], isfinite(gv) ? 0.0 : 1.0);
+        acc[2] = fma(xa, gv + qa, acc[2]);  // 2 f(x) = x^T (A x + 2 q)
     }
-    const int ops[2] = {1, 1};
-    if (grid_reduce_last<2>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
+    const int ops[3] = {1, 1, 0};
+    if (grid_reduce_last<3>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
         double L = st->L > 0.0 && isfinite(st->L) ? st->L : 1.0;
         st->L = L;
         st->alpha = 1.0 / L;
         st->resid = acc[0];
         st->iter = 0;
+        st->f_cur = 0.5 * acc[2];
+        st->fhist[0] = st->f_cur;
         if (acc[1] > 0.0) {
             st->nan = 1;
             st->done = 1;
@@ -96,76 +107,141 @@ __global__ void __launch_bounds__(RELCP_NT) k_lcp_init(int64_t nc, int64_t cap, 
     }
 }
 
-// One BB projected-gradient update (the gather half of iteration k).
+// One BB projected-gradient update (the gather half of iteration k), with a
+// nonmonotone (GLL) line search that makes plain BB globally convergent
+// (spectral projected gradient, reading R1):
+//   d = P(x - alpha g) - x,  f(x + t d) = f + t g.d + t^2/2 d.A d  (f quadratic,
+//   f(x) = 1/2 x^T A x + q^T x; the LCP is its KKT system), so
+//   the line search is closed form: t = 1 when
+//   f + g.d + 1/2 s.y <= max(last M f) + gamma g.d, else t = -g.d / s.y (the
+//   exact minimiser along d, which satisfies the Armijo test for gamma < 1/2).
+// The iterate lives in two slots (x_k, g_k) and (x+, g+ = A x+ + q): the pass
+// reads the current slot and writes the other one, and the parity bit flips.
+// A shortened step (t < 1) is not written back: the next K6 / K7 read both
+// slots and form x_k + t (x+ - x_k), g_k + t (g+ - g_k) on the fly (A is
+// linear), so the common t = 1 iteration moves exactly the bytes of plain BB.
 template <bool CR>
 __global__ void __launch_bounds__(RELCP_NT, CR ? ITER_MINB_CR : ITER_MINB) k_lcp_iter(int64_t nc, int64_t cap, const int32_t *__restrict__ ia,
                                                        const int32_t *__restrict__ ib, const double *__restrict__ n,
                                                        const double *__restrict__ ta, const double *__restrict__ tb,
                                                        int64_t rs, const double *__restrict__ rc,
                                                        const double *__restrict__ U, double s,
-                                                       const double *__restrict__ q, double *__restrict__ x,
-                                                       double *__restrict__ g, double *part, unsigned *counter,
+                                                       const double *__restrict__ q, double *xA, double *gA,
+                                                       double *xB, double *gB, double *part, unsigned *counter,
                                                        LcpState *st) {
-    __shared__ double sh[5 * 32];
+    __shared__ double sh[6 * 32];
     if (st->done) return;
     const double alpha = st->alpha;
-    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    const bool fix = st->fix != 0;
+    const double tl = st->t_ls;
+    const double *xc = st->par ? xB : xA, *gc = st->par ? gB : gA;
+    double *xw = st->par ? xA : xB, *gw = st->par ? gA : gB;  // the other slot: read (fix) then written
+    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    // ILP constraints per thread per trip: independent loads in flight
-    constexpr int ILP = CR ? ITER_ILP_CR : ITER_ILP;
-    for (int64_t a0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a0 < nc; a0 += ILP * stride) {
-        double xo[ILP], go[ILP], qv[ILP], rd[ILP];
+    // ILP constraints per thread per trip: independent loads in flight.  The
+    // rare blended pass (fix) runs one row per trip to keep the register
+    // budget of the common pass.
+    auto pass = [&](auto ilp_c, auto fix_c) {
+        constexpr int ILP = decltype(ilp_c)::value;
+        constexpr bool FIX = decltype(fix_c)::value;
+        for (int64_t a0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a0 < nc; a0 += ILP * stride) {
+            double xo[ILP], go[ILP], qv[ILP], rd[ILP];
 #pragma unroll
-        for (int u = 0; u < ILP; ++u) {
-            const int64_t a = a0 + u * stride;
-            const bool ok = a < nc;
-            const int64_t ac = ok ? a : a0;
-            xo[u] = x[ac];
-            go[u] = g[ac];
-            qv[u] = q[ac];
-            rd[u] = ROW_DOT(ac);
-        }
+            for (int u = 0; u < ILP; ++u) {
+                const int64_t a = a0 + u * stride;
+                const bool ok = a < nc;
+                const int64_t ac = ok ? a : a0;
+                xo[u] = xc[ac];
+                go[u] = gc[ac];
+                if (FIX) {  // current iterate = blend of the two slots
+                    const double xp = xw[ac], gp = gw[ac];
+                    xo[u] = fma(tl, xo[u] - xp, xp);
+                    go[u] = fma(tl, go[u] - gp, gp);
+                }
+                qv[u] = q[ac];
+                rd[u] = ROW_DOT(ac);
+            }
 #pragma unroll
-        for (int u = 0; u < ILP; ++u) {
-            const int64_t a = a0 + u * stride;
-            if (a >= nc) continue;
-            const double xn = fmax(0.0, xo[u] - alpha * go[u]);
-            const double gn = fma(s, rd[u], qv[u]);
-            x[a] = xn;
-            g[a] = gn;
-            const double sd = xn - xo[u], yd = gn - go[u];
-            acc[0] = fma(sd, sd, acc[0]);
-            acc[1] = fma(sd, yd, acc[1]);
-            acc[2] = fma(yd, yd, acc[2]);
-            acc[3] = fmax(acc[3], fabs(fmin(xn, gn)));
-            acc[4] = fmax(acc[4], isfinite(gn) ? 0.0 : 1.0);
+            for (int u = 0; u < ILP; ++u) {
+                const int64_t a = a0 + u * stride;
+                if (a >= nc) continue;
+                const double xn = fmax(0.0, xo[u] - alpha * go[u]);
+                const double gn = fma(s, rd[u], qv[u]);
+                xw[a] = xn;
+                gw[a] = gn;
+                const double sd = xn - xo[u], yd = gn - go[u];
+                acc[0] = fma(sd, sd, acc[0]);
+                acc[1] = fma(sd, yd, acc[1]);
+                acc[2] = fma(yd, yd, acc[2]);
+                acc[3] = fmax(acc[3], fabs(fmin(xn, gn)));
+                acc[4] = fmax(acc[4], isfinite(gn) ? 0.0 : 1.0);
+                acc[5] = fma(go[u], sd, acc[5]);
+            }
         }
-    }
-    const int ops[5] = {0, 0, 0, 1, 1};
-    if (grid_reduce_last<5>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
+    };
+    if (fix)
+        pass(std::integral_constant<int, 1>{}, std::true_type{});
+    else
+        pass(std::integral_constant<int, CR ? ITER_ILP_CR : ITER_ILP>{}, std::false_type{});
+    const int ops[6] = {0, 0, 0, 1, 1, 0};
+    if (grid_reduce_last<6>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
         const long long k = st->iter;
         st->ss = acc[0];
         st->sy = acc[1];
         st->yy = acc[2];
         st->resid = acc[3];
-        if (acc[4] > 0.0 || !isfinite(acc[0]) || !isfinite(acc[1]) || !isfinite(acc[2])) {
+        st->iter = k + 1;
+        if (acc[4] > 0.0 || !isfinite(acc[0]) || !isfinite(acc[1]) || !isfinite(acc[2]) || !isfinite(acc[5])) {
             st->nan = 1;
             st->done = 1;
-            st->iter = k + 1;
             return;
         }
-        if (acc[3] <= st->tol) {
+        st->par ^= 1;  // (x+, g+) is the written slot
+        if (acc[3] <= st->tol) {  // the full step solves the LCP
+            st->fix = 0;
             st->conv = 1;
             st->done = 1;
-            st->iter = k + 1;
             return;
         }
-        if (acc[1] <= 0.0 || acc[2] == 0.0)
-            st->alpha = 1.0 / st->L;
-        else
-            st->alpha = (k % 2 == 0) ? acc[0] / acc[1] : acc[1] / acc[2];
-        st->iter = k + 1;
+        // nonmonotone line search along d = x+ - x (closed form, f quadratic)
+        const double gd = acc[5], dAd = acc[1];
+        double fmaxh = st->f_cur;
+#pragma unroll
+        for (int m = 0; m < RELCP_GLL_M; ++m) fmaxh = fmax(fmaxh, st->fhist[m]);
+        double t = 1.0;
+        if (!(st->f_cur + gd + 0.5 * dAd <= fmaxh + 1e-4 * gd) && dAd > 0.0) t = fmin(1.0, -gd / dAd);
+        st->f_cur += t * gd + 0.5 * t * t * dAd;
+        st->fhist[(k + 1) % RELCP_GLL_M] = st->f_cur;
+        st->fix = t < 1.0;
+        st->t_ls = t;
+        st->n_ls += t < 1.0;
+        // BB steps are invariant under the scaling s, y -> t s, t y
+        double al = (acc[1] <= 0.0 || acc[2] == 0.0) ? 1.0 / st->L : ((k % 2 == 0) ? acc[0] / acc[1] : acc[1] / acc[2]);
+        const double lo = 1e-10 / st->L, hi = 1e10 / st->L;
+        st->alpha = fmin(hi, fmax(lo, al));
         if (k + 1 >= st->max_iter) st->done = 1;
+    }
+}
+
+// After a BB solve that ended on a shortened step (fix): the iterate is the
+// blend of the two slots; write it into (x, g) and recompute the residual.
+__global__ void __launch_bounds__(RELCP_NT) k_bb_finish(int64_t nc, double *x, double *g, const double *xo,
+                                                        const double *go, double *part, unsigned *counter,
+                                                        LcpState *st) {
+    __shared__ double sh[32];
+    const double tl = st->t_ls;
+    double acc[1] = {0.0};
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
+        const double xv = fma(tl, x[a] - xo[a], xo[a]), gv = fma(tl, g[a] - go[a], go[a]);
+        x[a] = xv;
+        g[a] = gv;
+        acc[0] = fmax(acc[0], fabs(fmin(xv, gv)));
+    }
+    const int ops[1] = {1};
+    if (grid_reduce_last<1>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
+        st->resid = acc[0];
+        st->fix = 0;
+        st->conv = acc[0] <= st->tol;
     }
 }
 
@@ -309,6 +385,14 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
         k_apgd_setup<<<1, 1, 0, st>>>(ctx->st.p);
         CKL();
     }
+    const bool bb = !apgd && !fused;
+    if (bb) {
+        // second slot for (x+, g+) (k_lcp_iter); nothing to initialise: the
+        // first pass reads slot A = (lambda, g) and writes it
+        CK(ctx->apgd_buf.grow(2 * nc));
+        xB = ctx->apgd_buf.p;
+        gB = ctx->apgd_buf.p + nc;
+    }
     if (apgd) {
         // second iterate buffer (x', g') = (x_0, g_0); theta = 1, beta = 0, t = 1/(1.1 L)
         CK(ctx->apgd_buf.grow(2 * nc));
@@ -362,11 +446,11 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
                 k_apgd_iter<false><<<gridi, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g, xB,
                                                                gB, ctx->partials.p, ctx->counter.p, ctx->st.p);
             else if (cr)
-                k_lcp_iter<true><<<gridi, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g,
-                                                             ctx->partials.p, ctx->counter.p, ctx->st.p);
+                k_lcp_iter<true><<<gridi, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g, xB,
+                                                             gB, ctx->partials.p, ctx->counter.p, ctx->st.p);
             else
-                k_lcp_iter<false><<<gridi, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g,
-                                                              ctx->partials.p, ctx->counter.p, ctx->st.p);
+                k_lcp_iter<false><<<gridi, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g, xB,
+                                                              gB, ctx->partials.p, ctx->counter.p, ctx->st.p);
             CKL();
             if (ev_on) CK(cudaEventRecord(ctx->ev[3 * j + 2], st));
         }
@@ -432,6 +516,18 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
         const cudaError_t e = cudaGraphExecDestroy(gexec);
         gexec = nullptr;
         CK(e);
+    }
+    if (bb && ctx->st_host->fix) {
+        // ended on a shortened step: the iterate is x_k + t (x+ - x_k), x+ in the
+        // current slot, x_k in the other one
+        const bool pb = ctx->st_host->par != 0;
+        k_bb_finish<<<gridc, RELCP_NT, 0, st>>>(nc, pb ? xB : cs->lambda, pb ? gB : cs->g, pb ? cs->lambda : xB,
+                                                pb ? cs->g : gB, ctx->partials.p, ctx->counter.p, ctx->st.p);
+        CKL();
+    }
+    if (bb && ctx->st_host->par) {  // the current BB iterate lives in the second slot
+        CK(cudaMemcpyAsync(cs->lambda, xB, sizeof(double) * nc, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(cs->g, gB, sizeof(double) * nc, cudaMemcpyDeviceToDevice, st));
     }
     if (apgd && ctx->st_host->par) {  // the current APGD iterate lives in the second buffer
         CK(cudaMemcpyAsync(cs->lambda, xB, sizeof(double) * nc, cudaMemcpyDeviceToDevice, st));

@@ -268,11 +268,21 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
     // contributions staged as 3 planes of double2 (components 01, 23, 45):
     // 128-bit shared loads in the per-lane segment sums
     __shared__ double2 sm[SCATTER_WPB][3][SCATTER_TILE + 1];
-    double alpha = 0.0, beta = 0.0;
+    double alpha = 0.0, beta = 0.0, tl = 1.0;
+    bool fix = false;
     const double *xc = x, *gc = g, *xp = xb, *gp = gb;
     if (MODE != 0) {
         if (st->done) return;
         alpha = st->alpha;
+    }
+    if (MODE == 1) {
+        // BB (lcp.cu k_lcp_iter): current slot by parity; after a shortened
+        // step the iterate is the blend xp + t (xc - xp) of the two slots
+        if (st->par) {
+            xc = xb; gc = gb; xp = x; gp = g;
+        }
+        fix = st->fix != 0;
+        tl = st->t_ls;
     }
     if (MODE == 2) {
         beta = st->beta;
@@ -290,7 +300,13 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
         if (MODE == 0 || MODE == 3) {
             xv = xc[c];
         } else if (MODE == 1) {
-            xv = fmax(0.0, xc[c] - alpha * gc[c]);
+            double x0 = xc[c], g0 = gc[c];
+            if (fix) {
+                const double xq = xp[c], gq = gp[c];
+                x0 = fma(tl, x0 - xq, xq);
+                g0 = fma(tl, g0 - gq, gq);
+            }
+            xv = fmax(0.0, x0 - alpha * g0);
         } else {
             const double x0 = xc[c], g0 = gc[c];
             const double y = x0 + beta * (x0 - xp[c]), gy = g0 + beta * (g0 - gp[c]);

@@ -54,10 +54,31 @@ __global__ void k_merge(int64_t n_old, int64_t total, int64_t cap, const int32_t
     }
 }
 
+// bad[0] = 1 if a (ia, ib) key decreases inside [0, n_old) or inside
+// [n_old, total) (the two runs the merge assumes sorted)
+__global__ void k_check_runs(int64_t n_old, int64_t total, const int32_t *__restrict__ ia,
+                             const int32_t *__restrict__ ib, int *bad) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a + 1 < total;
+         a += (int64_t)gridDim.x * blockDim.x)
+        if (a + 1 != n_old && row_key(ia, ib, a) > row_key(ia, ib, a + 1)) *bad = 1;
+}
+
 // Merge rows [n_old, n_old + m) (sorted) into the sorted rows [0, n_old).
+// A store whose runs are not (ia, ib)-sorted (a caller's own order, e.g. rows
+// loaded or edited out of order) is left as appended: the operator handles
+// any row order (general CSR path), only the fast sorted path is lost.
 int store_merge_appended(relcp_ctx *ctx, relcp_constraints *cs, int64_t n_old, int64_t m) {
     if (m <= 0 || n_old <= 0) return RELCP_OK;  // already sorted
     const int64_t total = n_old + m, cap = cs->capacity;
+    CK(ctx->red.grow(64));
+    CK(cudaMemsetAsync(ctx->red.p + 63, 0, sizeof(double), ctx->stream));
+    int *bad = reinterpret_cast<int *>(ctx->red.p + 63);
+    k_check_runs<<<grid_for(total), RELCP_NT, 0, ctx->stream>>>(n_old, total, cs->ia, cs->ib, bad);
+    CKL();
+    int bad_h = 0;
+    CK(cudaMemcpyAsync(&bad_h, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (bad_h) return RELCP_OK;
     CK(ctx->mi.grow(3 * total));
     CK(ctx->md.grow(13 * total));
     cudaStream_t st = ctx->stream;

@@ -143,3 +143,86 @@ def test_overdamped_force_balance(orc):
     f = U[:, :3] * L[:, None]
     assert np.abs(f.sum(0)).max() <= 1e-10 * np.abs(f).sum()
     assert r["max_overlap"] <= sc["eps_ncp"]
+
+
+def _nonspherical_cluster(seed=21, n=64, dt=1e-3):
+    """Non-periodic cluster of non-spherical ellipsoids with distinct axes per
+    body (a = 1, b ~ U(0.45, 0.8), c ~ U(0.25, 0.42)), uniform orientations,
+    u, w ~ N(0, 1), overlapping neighbours; textbook solid-ellipsoid mass
+    properties (rho = 1)."""
+    sc = scenes.suspension(n, (1.0, 0.6, 0.4), 0.45, seed, dt=dt)
+    rng = np.random.default_rng(seed)
+    axes = np.stack([np.ones(n), rng.uniform(0.45, 0.8, n), rng.uniform(0.25, 0.42, n)], 1)
+    a, b, c = axes.T
+    m = 4.0 / 3.0 * math.pi * a * b * c
+    sc["axes"] = axes
+    sc["inv_mass"] = 1.0 / m
+    sc["inv_inertia"] = 1.0 / np.stack([m / 5 * (b * b + c * c), m / 5 * (a * a + c * c), m / 5 * (a * a + b * b)], 1)
+    sc["box"] = np.zeros(3)
+    return sc
+
+
+def _world_inertia(quat, inv_inertia):
+    """I_world = R diag(I_body) R^T, R the rotation of the unit quaternion
+    (s, w): R = I + 2 s [w]x + 2 [w]x^2 (textbook, written here independently)."""
+    q = quat / np.linalg.norm(quat, axis=1, keepdims=True)
+    s, w = q[:, 0], q[:, 1:]
+    K = np.zeros((len(q), 3, 3))
+    K[:, 0, 1], K[:, 0, 2], K[:, 1, 2] = -w[:, 2], w[:, 1], -w[:, 0]
+    K[:, 1, 0], K[:, 2, 0], K[:, 2, 1] = w[:, 2], -w[:, 1], w[:, 0]
+    R = np.eye(3) + 2 * s[:, None, None] * K + 2 * K @ K
+    return np.einsum("nij,nj,nkj->nik", R, 1.0 / inv_inertia, R)
+
+
+def _angular_momentum_defect(O, sc, **kw):
+    """|Delta L| / scale over the step, L = sum m x^k x u + I_world(C^k) omega
+    about the origin (first-order scheme: momenta at C^k)."""
+    r = O.relcp_step(sc, lcp_tol=1e-12, **kw)
+    m = 1.0 / sc["inv_mass"]
+    Iw = _world_inertia(sc["quat"], sc["inv_inertia"])
+    du = r["vel"] - sc["vel"]
+    lin = m[:, None] * np.cross(sc["pos"], du[:, :3])
+    ang = np.einsum("nij,nj->ni", Iw, du[:, 3:])
+    scale = np.abs(lin).sum() + np.abs(ang).sum()
+    return np.abs((lin + ang).sum(0)).max() / scale, r, scale
+
+
+def _relaxed_subcluster():
+    """The overlap-free cfg1-relaxed bodies (tests/golden, oracle-made) as a
+    NON-periodic cluster (contacts across the periodic faces dropped)."""
+    sc = scenes.cfg1_relaxed(dt=1e-3)
+    sc["box"] = np.zeros(3)
+    return sc
+
+
+@pytest.mark.parametrize("case", ["cluster-snsd-lcp", "relaxed-relcp"])
+def test_angular_momentum_conserved(orc, case, monkeypatch):
+    """F_ext = 0, inertial, non-periodic: the contact impulses -gamma n on a at
+    y_a and +gamma n on b at y_b act along the common normal line
+    (y_b - y_a = Phi n; F_a = -n gamma, T_a = -(y_a - x_a) x n gamma,
+    P:L151-157), so its moment about the origin, (y_b - y_a) x n gamma,
+    vanishes and sum(m x x u + R I R^T omega) is unchanged for rows discovered
+    at C^k: the LCP-SNSD step of a deeply overlapping cluster with distinct
+    axes per body, and the ReLCP step of an overlap-free (relaxed) cluster,
+    which appends no rows (Cor. 4).  The same check
+    on an oracle whose rotational mobility is transposed (R^T I^-1 R instead of
+    R I^-1 R^T) must fail: this pins the inertial W block."""
+    snsd_only = case == "cluster-snsd-lcp"
+    sc = _nonspherical_cluster() if snsd_only else _relaxed_subcluster()
+    defect, r, scale = _angular_momentum_defect(orc, sc, snsd_only=snsd_only)
+    assert r["recursions"] == 0 and len(r["constraints"]["ia"]) > 20
+    assert np.abs(r["constraints"]["lam"]).max() > 0 and scale > 1e-3
+    assert defect <= 1e-12, defect
+
+    real = orc.body_W
+
+    def transposed(s, quat=None):
+        W = real(s, quat).reshape(-1, 6, 6)
+        W[:, 3:, 3:] = np.swapaxes(W[:, 3:, 3:], 1, 2)  # symmetric: no change
+        R = orc.quat_to_rot(s["quat"] if quat is None else quat)
+        W[:, 3:, 3:] = np.einsum("nji,nj,njk->nik", R, s["inv_inertia"], R)  # R^T I^-1 R
+        return W.reshape(-1, 36)
+
+    monkeypatch.setattr(orc, "body_W", transposed)
+    bad, _, _ = _angular_momentum_defect(orc, sc, snsd_only=snsd_only)
+    assert bad > 1e-6, bad

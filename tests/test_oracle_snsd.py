@@ -215,3 +215,86 @@ def test_cfg1_pair_counts_and_degenerate(orc):
     assert 300 < (phi < 0.1).sum() < 600
     _, _, _, _, st = orc.snsd(np.zeros((2, 3)), np.array([[1, 0, 0, 0.0]] * 2), np.ones((2, 3)), None, [0], [1])
     assert st[0] == 1
+
+
+def _fib(N):
+    k = np.arange(N) + 0.5
+    z = 1 - 2 * k / N
+    r = np.sqrt(1 - z * z)
+    th = math.pi * (3 - math.sqrt(5)) * k
+    return np.stack([r * np.cos(th), r * np.sin(th), z], 1)
+
+
+def _overlap_family_pairs(rng, P):
+    """Overlapping, NON-identical pairs (independent orientations) of the
+    BASELINE shape families: cfg5 (1, 0.6, 0.4), cfg2 (1, 1/r, 1/r) with
+    aspect ratio r up to 4, cfg1 (1, 0.5, 0.5), and cfg5 vs cfg2 mixed;
+    centre offsets from moderate to deep (|d| ~ U(0.02, 1.6))."""
+    fam = rng.integers(0, 4, P)
+
+    def shape(f):
+        if f == 0:
+            return [1.0, 0.6, 0.4]
+        if f == 1:
+            r = rng.uniform(1.0, 4.0)
+            return [1.0, 1.0 / r, 1.0 / r]
+        return [1.0, 0.5, 0.5]
+
+    axes = []
+    for f in fam:
+        axes += [shape(0), shape(1)] if f == 3 else [shape(f), shape(f)]
+    axes = np.array(axes)
+    quat = rng.standard_normal((2 * P, 4))
+    pos = np.zeros((2 * P, 3))
+    d = rng.standard_normal((P, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    pos[1::2] = d * np.where(rng.uniform(size=(P, 1)) < 0.5, rng.uniform(0.02, 0.7, (P, 1)),
+                             rng.uniform(0.7, 1.6, (P, 1)))
+    return pos, quat, axes, np.arange(0, 2 * P, 2), np.arange(1, 2 * P, 2)
+
+
+def test_snsd_overlap_global_max_dense_directions(orc):
+    """Phi = max_{|n|=1} f(n), f(n) = n.d - h_a(n) - h_b(n) (P:L225,
+    P:L678-680) for >= 200 overlapping non-identical pairs, against a brute
+    force over 10^6 Fibonacci directions evaluated from the definition
+    (Sigma = R diag(e^2) R^T, h = sqrt(n^T Sigma n), written out here):
+      * Phi_bf <= Phi + 1e-12: no sampled direction beats the oracle's maximum
+        (a missed global maximum shows up here);
+      * Phi - Phi_bf <= L_f delta: the sample comes within its covering radius
+        delta of the maximiser, |grad f| <= L_f = |d| + max e_a + max e_b.
+    The same check on the single-start (d/|d| only) variant of the oracle's
+    Newton must FAIL on some deep overlaps: the pin sees a lost multistart."""
+    rng = np.random.default_rng(17)
+    pos, quat, axes, pi, pj = _overlap_family_pairs(rng, 320)
+    phi, n, ra, rb, st = orc.snsd(pos, quat, axes, None, pi, pj)
+    phi1, *_ = orc.snsd(pos, quat, axes, None, pi, pj, n_fib=0)  # d/|d| start only
+    ov = phi < 0
+    assert ov.sum() >= 200 and np.all(st[ov] == 0)
+    N = 1_000_000
+    U = _fib(N)
+    Q = np.stack([U[:, 0] ** 2, U[:, 1] ** 2, U[:, 2] ** 2, 2 * U[:, 0] * U[:, 1], 2 * U[:, 0] * U[:, 2],
+                  2 * U[:, 1] * U[:, 2]], 1)
+    q = quat / np.linalg.norm(quat, axis=1, keepdims=True)
+    s, w = q[:, 0], q[:, 1:]
+    K = np.zeros((len(q), 3, 3))
+    K[:, 0, 1], K[:, 0, 2], K[:, 1, 2] = -w[:, 2], w[:, 1], -w[:, 0]
+    K[:, 1, 0], K[:, 2, 0], K[:, 2, 1] = w[:, 2], -w[:, 1], w[:, 0]
+    R = np.eye(3) + 2 * s[:, None, None] * K + 2 * K @ K
+    S = np.einsum("nik,nk,njk->nij", R, axes ** 2, R)
+    sv = np.stack([S[:, 0, 0], S[:, 1, 1], S[:, 2, 2], S[:, 0, 1], S[:, 0, 2], S[:, 1, 2]], 1)
+    d = pos[pj] - pos[pi]
+    bf = np.empty(len(pi))
+    for c in range(0, len(pi), 16):
+        sl = slice(c, c + 16)
+        f = U @ d[sl].T - np.sqrt(Q @ sv[pi[sl]].T) - np.sqrt(Q @ sv[pj[sl]].T)
+        bf[sl] = f.max(0)
+    # covering radius of the direction sample: farthest of 2e5 random probes
+    probe = rng.standard_normal((200_000, 3))
+    probe /= np.linalg.norm(probe, axis=1, keepdims=True)
+    chord, _ = cKDTree(U).query(probe, k=1)
+    delta = 2.0 * np.arcsin(chord.max() / 2.0) * 1.25
+    Lf = np.linalg.norm(d, axis=1) + axes[pi].max(1) + axes[pj].max(1)
+    assert np.all(bf[ov] <= phi[ov] + 1e-12), (bf - phi)[ov].max()
+    assert np.all(phi[ov] - bf[ov] <= Lf[ov] * delta)
+    assert np.max(phi[ov] - bf[ov]) < 1e-4  # the sample's actual miss is O(delta^2)
+    assert np.any(bf[ov] > phi1[ov] + 1e-6), "d/|d|-only Newton passed: the pin is blind to the multistart"
