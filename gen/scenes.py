@@ -144,6 +144,17 @@ def cfg5(seed: int = 5, n: int = 2_000_000) -> dict:
                       dynamics=INERTIAL, name="cfg5" if n == 2_000_000 else f"cfg5-n{n}")
 
 
+def with_state(sc: dict, pos, quat, vel_seed: int, name: str) -> dict:
+    """A "-relaxed" companion: the scene's bodies at a given
+    (relaxed) configuration with fresh u, w ~ N(0, 1) from PCG64(vel_seed).
+    Draws only; the configuration comes from the caller (the cfg5-relaxed
+    state is relaxed by the library itself, bench.py / drivers.relax)."""
+    out = dict(sc)
+    out.update(pos=np.ascontiguousarray(pos, dtype=np.float64), quat=np.ascontiguousarray(quat, dtype=np.float64),
+               vel=np.random.Generator(np.random.PCG64(vel_seed)).standard_normal((sc["n"], 6)), name=name)
+    return out
+
+
 def colony_rods(seed: int = 7, n: int = 131_072, dt: float = 1e-2, patch: int = 6) -> dict:
     """The paper's colony shape class: spherocylinders
     of diameter b = 0.5 and centreline length l ~ U(2, 4) (between l_0 and the
@@ -385,6 +396,30 @@ def random_constraint_network(n_bodies: int, n_con: int, seed: int,
     same = ia == ib
     ib[same] = (ib[same] + 1) % n_bodies
     lo, hi = np.minimum(ia, ib), np.maximum(ia, ib)
+    order = np.lexsort((hi, lo))
+    ia, ib = lo[order].astype(np.int32), hi[order].astype(np.int32)
+    nrm = rng.standard_normal((n_con, 3))
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    ra = rng.uniform(-0.7, 0.7, size=(n_con, 3))
+    rb = rng.uniform(-0.7, 0.7, size=(n_con, 3))
+    return b, ia, ib, nrm, ra, rb
+
+
+def local_constraint_network(n_bodies: int, n_con: int, seed: int, dynamics: int = INERTIAL):
+    """Spatially local random Jacobian data at a given size (timing inputs for
+    the CPU oracle at cfg5's N and N_C, bench.py cpu_baseline): the cfg5
+    suspension's bodies (jittered lattice, phi = 0.55, kept in lattice order)
+    and rows between a body and a lattice neighbour (index offset 1, n_side or
+    n_side^2, as contacts of the lattice-ordered cfg5 bodies are), unit
+    normals, lever arms |r_i| <= 0.7.  Returns bodies dict + (ia, ib, n, ra, rb)
+    sorted by (ia, ib)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    b = suspension(n_bodies, (1.0, 0.6, 0.4), 0.55, seed + 1000, dynamics=dynamics)
+    n_side = int(math.ceil(round(n_bodies ** (1.0 / 3.0), 9)))
+    a = rng.integers(0, n_bodies, size=n_con)
+    off = np.array([1, n_side, n_side * n_side])[rng.integers(0, 3, size=n_con)]
+    c = (a + off) % n_bodies
+    lo, hi = np.minimum(a, c), np.maximum(a, c)
     order = np.lexsort((hi, lo))
     ia, ib = lo[order].astype(np.int32), hi[order].astype(np.int32)
     nrm = rng.standard_normal((n_con, 3))

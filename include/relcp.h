@@ -176,6 +176,11 @@ typedef struct relcp_step_report {
     double f_n[RELCP_MAX_REC];          /* f_n = -1/2 x^T A_n x        */
     double ms_generate, ms_solve, ms_check; /* wall time per phase (events)      */
     int64_t snsd_nonconv;               /* SNSD solves not certified (all calls) */
+    int64_t n_guard;                    /* pairs of this step's SNSD scans with   */
+                                        /* |Phi - threshold| < 1e-10 (cutoff at   */
+                                        /* generation, -eps_ncp at checks): the   */
+                                        /* R14 guard band, where another correct  */
+                                        /* fp64 code may decide the other way     */
 } relcp_step_report;
 
 /* ---------------------------------------------------------------- context */
@@ -286,7 +291,11 @@ int relcp_get_pairs(relcp_ctx *ctx, int32_t *pi, int32_t *pj, int64_t cap, int64
  *                           (events around the graph launch);
  *   scatter_ms / gather_ms  summed K6 / K7 (or fused row pass / b-side scatter)
  *                           durations over the split_timed iterations of the
- *                           direct batches. */
+ *                           direct batches;
+ *   n_guard                 SNSD-scanned pairs inside the R14 guard band
+ *                           |Phi - threshold| < 1e-10 (generation: cutoff;
+ *                           checks: -eps_ncp), over every generate / check
+ *                           since the reset (timing off or on). */
 typedef struct relcp_stats {
     int64_t launches;
     int64_t lcp_iterations;
@@ -295,6 +304,7 @@ typedef struct relcp_stats {
     double gather_ms;
     int64_t split_timed;
     double iter_ms;
+    int64_t n_guard;
 } relcp_stats;
 int relcp_get_stats(relcp_ctx *ctx, relcp_stats *out);
 int relcp_reset_stats(relcp_ctx *ctx);
@@ -305,6 +315,61 @@ int relcp_set_timing(relcp_ctx *ctx, int32_t on);
  * (P) int32 0 ok / 1 coincident centres / 2 not certified.  Asynchronous. */
 int relcp_snsd_pairs(relcp_ctx *ctx, const relcp_bodies *bodies, int64_t n_pairs, const int32_t *pi,
                      const int32_t *pj, double *phi, double *nrm, double *ra, double *rb, int32_t *status);
+
+/* ------------------------------------------------ domain decomposition
+ * SURVEY §8(e) / §8(f) rank 4 (the paper's solver is distributed over spatial
+ * domains with MPI).  Bodies are split into K contiguous index ranges
+ * [part_off[k], part_off[k+1]) (part_off[0] = 0, part_off[K] = n); constraint
+ * alpha belongs to the part owning ia (rows must be sorted by ia, R18, so a
+ * part's rows are one contiguous range [row_lo, row_hi)); a part's ghosts are
+ * the ib of its rows owned elsewhere.  Per apply / BB iteration the ghost
+ * partial wrenches go to their owners, which add them in ascending part order
+ * (deterministic, no atomics) before applying W, and the owners' U go back to
+ * the ghost slots (48 B per boundary body and direction); the BB dot products
+ * and residual are combined over the parts (fixed part order, or one grouped
+ * NCCL all-reduce of <= 6 doubles).  DESIGN.md §8. */
+typedef struct relcp_dd relcp_dd;
+typedef struct relcp_dd_info {
+    int64_t n_own;      /* owned bodies                                   */
+    int64_t n_ghost;    /* ghost bodies (ib of owned rows owned elsewhere) */
+    int64_t row_lo, row_hi; /* owned rows of the ia-sorted store          */
+    int64_t n_recv;     /* halo slots received (ghost partials of others) */
+    int64_t n_boundary; /* owned bodies that receive halo partials        */
+} relcp_dd_info;
+
+/* Host-only partition plan of part `part` (no device needed): info, and when
+ * non-NULL ghost[n_ghost] (global ids, ascending), gseg[K+1] (ghost segment of
+ * each owner part), rseg[K+1] (receive-slot segment of each source part),
+ * recv_list[n_recv] (owned local id of each receive slot; the slots of source
+ * p hold p's ghosts owned here, in p's ghost order).  ia/ib: host arrays.
+ * Errors: E_ARG (bad offsets, rows not sorted by ia, ia == ib, ids out of range). */
+int relcp_dd_plan_host(int32_t nparts, const int64_t *part_off, int64_t nc, const int32_t *ia, const int32_t *ib,
+                       int32_t part, relcp_dd_info *info, int64_t *ghost, int64_t *gseg, int64_t *rseg,
+                       int32_t *recv_list);
+/* 128-byte NCCL unique id for relcp_dd_create in NCCL mode (rank 0 makes it,
+ * the caller broadcasts it).  E_CUDA if libnccl.so.2 cannot be loaded. */
+int relcp_dd_nccl_unique_id(void *out128);
+/* rank < 0: VIRTUAL mode, all K parts in this process on this device (halo
+ * exchange by device copies).  rank >= 0: NCCL mode, this process holds part
+ * `rank` of K ranks (one GPU each; nccl_uid from relcp_dd_nccl_unique_id). */
+int relcp_dd_create(relcp_dd **out, const relcp_params *p, void *cuda_stream, int32_t nparts,
+                    const int64_t *part_off, int32_t rank, const void *nccl_uid);
+int relcp_dd_destroy(relcp_dd *dd);
+const char *relcp_dd_last_error(const relcp_dd *dd);
+/* Partition (bodies, constraints) -- global device arrays as in relcp_prepare_
+ * operator; the store must stay in place (q / lambda / g are used through
+ * views) until the next load.  Synchronises. */
+int relcp_dd_load(relcp_dd *dd, const relcp_bodies *bodies, const relcp_constraints *cs);
+int relcp_dd_info_get(relcp_dd *dd, int32_t part, relcp_dd_info *info);
+/* y = scale D^T W D x over the parts (x, y: device, global row order; NCCL
+ * mode writes this rank's rows only).  Asynchronous. */
+int relcp_dd_delassus_apply(relcp_dd *dd, const double *x, double *y, double scale);
+/* U (n, 6) of the owned bodies of the local parts after the last apply /
+ * solve, into a global (n, 6) device array.  Asynchronous. */
+int relcp_dd_get_u(relcp_dd *dd, double *U);
+/* relcp_solve_lcp over the parts (BB, same parameters); cs = the loaded store.
+ * Returns OK, W_MAX_ITER or E_NAN like relcp_solve_lcp.  Synchronises. */
+int relcp_dd_solve_lcp(relcp_dd *dd, relcp_constraints *cs, relcp_solve_report *rep);
 
 #ifdef __cplusplus
 }

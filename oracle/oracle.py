@@ -35,42 +35,54 @@ LIB = os.path.join(HERE, "liboracle.so")
 INERTIAL = 0
 OVERDAMPED = 1
 _lib = None
+LIB_OMP = os.path.join(HERE, "liboracle_omp.so")
+_lib_omp = None
 
 
-def build(force: bool = False) -> str:
-    """Compile relcp_oracle.c with gcc (no FMA contraction, no fast-math)."""
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+def build(force: bool = False, openmp: bool = False) -> str:
+    """Compile relcp_oracle.c with gcc (no FMA contraction, no fast-math).
+    openmp=True builds the timing-only all-core variant liboracle_omp.so
+    (bench.py cpu_baseline); every test uses the serial liboracle.so."""
+    out = LIB_OMP if openmp else LIB
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(SRC):
         subprocess.check_call(["gcc", "-O2", "-std=gnu99", "-ffp-contract=off", "-fno-fast-math",
-                               "-shared", "-fPIC", "-o", LIB, SRC, "-lm"])
-    return LIB
+                               *(["-fopenmp"] if openmp else []), "-shared", "-fPIC", "-o", out, SRC, "-lm"])
+    return out
 
 
-def lib():
-    global _lib
+def lib(openmp: bool = False):
+    global _lib, _lib_omp
+    if openmp:
+        if _lib_omp is None:
+            _lib_omp = _load(build(openmp=True))
+        return _lib_omp
     if _lib is None:
-        build()
-        L = ctypes.CDLL(LIB)
-        P = ctypes.c_void_p
-        i64 = ctypes.c_int64
-        L.orc_snsd_batch.restype = i64
-        L.orc_snsd_batch.argtypes = [i64, P, P, P, P, P, P, ctypes.c_int, P, P, P, P, P]
-        L.orc_snsd_batch_shapes.restype = i64
-        L.orc_snsd_batch_shapes.argtypes = [i64, P, P, P, P, P, P, P, ctypes.c_int, P, P, P, P, P]
-        L.orc_broadphase_bruteforce.restype = i64
-        L.orc_broadphase_bruteforce.argtypes = [i64, P, P, P, ctypes.c_double, P, P, i64]
-        L.orc_broadphase_cells.restype = i64
-        L.orc_broadphase_cells.argtypes = [i64, P, P, P, ctypes.c_double, P, P, i64]
-        L.orc_delassus_apply.restype = None
-        L.orc_delassus_apply.argtypes = [i64, i64, P, P, P, P, P, P, ctypes.c_double, P, P]
-        L.orc_wrench.restype = None
-        L.orc_wrench.argtypes = [i64, i64, P, P, P, P, P, P, P, P, P]
-        L.orc_bbpgd.restype = None
-        L.orc_bbpgd.argtypes = [i64, i64, P, P, P, P, P, P, ctypes.c_double, P, P, P,
-                                ctypes.c_double, i64, ctypes.c_int, P]
-        L.orc_pgs_csr.restype = None
-        L.orc_pgs_csr.argtypes = [i64, P, P, P, P, P, P, ctypes.c_double, i64, P]
-        _lib = L
+        _lib = _load(build())
     return _lib
+
+
+def _load(path):
+    L = ctypes.CDLL(path)
+    P = ctypes.c_void_p
+    i64 = ctypes.c_int64
+    L.orc_snsd_batch.restype = i64
+    L.orc_snsd_batch.argtypes = [i64, P, P, P, P, P, P, ctypes.c_int, P, P, P, P, P]
+    L.orc_snsd_batch_shapes.restype = i64
+    L.orc_snsd_batch_shapes.argtypes = [i64, P, P, P, P, P, P, P, ctypes.c_int, P, P, P, P, P]
+    L.orc_broadphase_bruteforce.restype = i64
+    L.orc_broadphase_bruteforce.argtypes = [i64, P, P, P, ctypes.c_double, P, P, i64]
+    L.orc_broadphase_cells.restype = i64
+    L.orc_broadphase_cells.argtypes = [i64, P, P, P, ctypes.c_double, P, P, i64]
+    L.orc_delassus_apply.restype = None
+    L.orc_delassus_apply.argtypes = [i64, i64, P, P, P, P, P, P, ctypes.c_double, P, P]
+    L.orc_wrench.restype = None
+    L.orc_wrench.argtypes = [i64, i64, P, P, P, P, P, P, P, P, P]
+    L.orc_bbpgd.restype = None
+    L.orc_bbpgd.argtypes = [i64, i64, P, P, P, P, P, P, ctypes.c_double, P, P, P,
+                            ctypes.c_double, i64, ctypes.c_int, P]
+    L.orc_pgs_csr.restype = None
+    L.orc_pgs_csr.argtypes = [i64, P, P, P, P, P, P, ctypes.c_double, i64, P]
+    return L
 
 
 def _p(a):
@@ -195,15 +207,16 @@ def rows(nrm, ra, rb):
     return np.cross(ra, nrm), np.cross(rb, nrm)
 
 
-def delassus_apply(W, ia, ib, nrm, ta, tb, s, x):
-    """y = s D^T W D x (plain definition; long-double accumulation in C)."""
+def delassus_apply(W, ia, ib, nrm, ta, tb, s, x, openmp: bool = False):
+    """y = s D^T W D x (plain definition; long-double accumulation in C).
+    openmp=True: the timing-only all-core build (bench.py cpu_baseline)."""
     nb = W.shape[0]
     nc = len(ia)
     W, nrm, ta, tb = (_c(a, np.float64) for a in (W, nrm, ta, tb))
     ia, ib = _c(ia, np.int32), _c(ib, np.int32)
     x = _c(x, np.float64)
     y = np.empty(nc)
-    lib().orc_delassus_apply(nb, nc, _p(ia), _p(ib), _p(nrm), _p(ta), _p(tb), _p(W), float(s),
+    lib(openmp).orc_delassus_apply(nb, nc, _p(ia), _p(ib), _p(nrm), _p(ta), _p(tb), _p(W), float(s),
                              _p(x), _p(y))
     return y
 
@@ -219,9 +232,11 @@ def wrench(W, ia, ib, nrm, ta, tb, x):
     return F, U
 
 
-def bbpgd(W, ia, ib, nrm, ta, tb, s, q, x0=None, tol=1e-10, max_iter=1_000_000, power_iters=20):
+def bbpgd(W, ia, ib, nrm, ta, tb, s, q, x0=None, tol=1e-10, max_iter=1_000_000, power_iters=20,
+          openmp: bool = False):
     """Solve 0 <= A x + q _|_ x >= 0, A = s D^T W D (Lemma 3) by
-    BB projected gradient (reading R1).  Returns x, g, info dict."""
+    BB projected gradient (reading R1).  Returns x, g, info dict.
+    openmp=True: the timing-only all-core build (bench.py cpu_baseline)."""
     nb = W.shape[0]
     nc = len(ia)
     W, nrm, ta, tb, q = (_c(a, np.float64) for a in (W, nrm, ta, tb, q))
@@ -229,7 +244,7 @@ def bbpgd(W, ia, ib, nrm, ta, tb, s, q, x0=None, tol=1e-10, max_iter=1_000_000, 
     x = np.zeros(nc) if x0 is None else _c(x0, np.float64).copy()
     g = np.empty(nc)
     info = np.zeros(4)
-    lib().orc_bbpgd(nb, nc, _p(ia), _p(ib), _p(nrm), _p(ta), _p(tb), _p(W), float(s), _p(q), _p(x),
+    lib(openmp).orc_bbpgd(nb, nc, _p(ia), _p(ib), _p(nrm), _p(ta), _p(tb), _p(W), float(s), _p(q), _p(x),
                     _p(g), float(tol), int(max_iter), int(power_iters), _p(info))
     return x, g, dict(iterations=int(info[0]), residual=float(info[1]), converged=bool(info[2]),
                       L=float(info[3]))

@@ -29,6 +29,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #define ORC_OK 0
 #define ORC_DEGENERATE 1
@@ -38,6 +41,20 @@
 
 /* Rotation matrix of the unit quaternion q = (s, w), row-major,
  * R = I + 2 s [w]x + 2 [w]x^2 after normalising q. */
+/* Timing-only OpenMP build (bench.py cpu_baseline, "-fopenmp" -> liboracle_omp.so):
+ * the independent per-body / per-row loops of the apply and of the BB vector
+ * updates run on all host cores; in the apply's wrench scatter each thread
+ * adds the terms of its own body range in the serial alpha order.  The test
+ * oracle (liboracle.so) is compiled WITHOUT -fopenmp, so these pragmas are
+ * empty there and its arithmetic is the serial code below. */
+#ifdef _OPENMP
+#define ORC_OMP_FOR _Pragma("omp parallel for schedule(static)")
+#define ORC_OMP_FOR_REDUCE _Pragma("omp parallel for schedule(static) reduction(+ : ss, sy, yy) reduction(max : r)")
+#else
+#define ORC_OMP_FOR
+#define ORC_OMP_FOR_REDUCE
+#endif
+
 static void quat_to_rot(const double q_in[4], double R[9]) {
     double nq = sqrt(q_in[0] * q_in[0] + q_in[1] * q_in[1] + q_in[2] * q_in[2] +
                      q_in[3] * q_in[3]);
@@ -600,6 +617,26 @@ void orc_delassus_apply(int64_t nb, int64_t nc, const int32_t *ia, const int32_t
                         double *y) {
     long double *F = calloc((size_t)(6 * nb), sizeof(long double));
     long double *U = calloc((size_t)(6 * nb), sizeof(long double));
+#ifdef _OPENMP
+    /* timing build: thread t owns bodies [lo, hi) and adds, in the same
+     * alpha order, only the wrench terms of its own bodies (same sums) */
+#pragma omp parallel
+    {
+        const int64_t T = omp_get_num_threads(), t = omp_get_thread_num();
+        const int64_t lo = nb * t / T, hi = nb * (t + 1) / T;
+        for (int64_t al = 0; al < nc; ++al) {
+            long double xa = x[al];
+            int a = ia[al], b = ib[al];
+            const int own_a = a >= lo && a < hi, own_b = b >= lo && b < hi;
+            for (int k = 0; k < 3 && (own_a || own_b); ++k) {
+                if (own_a) F[6 * a + k] += -(long double)nrm[3 * al + k] * xa;
+                if (own_a) F[6 * a + 3 + k] += -(long double)ta[3 * al + k] * xa;
+                if (own_b) F[6 * b + k] += (long double)nrm[3 * al + k] * xa;
+                if (own_b) F[6 * b + 3 + k] += (long double)tb[3 * al + k] * xa;
+            }
+        }
+    }
+#else
     for (int64_t al = 0; al < nc; ++al) {
         long double xa = x[al];
         int a = ia[al], b = ib[al];
@@ -610,12 +647,15 @@ void orc_delassus_apply(int64_t nb, int64_t nc, const int32_t *ia, const int32_t
             F[6 * b + 3 + k] += (long double)tb[3 * al + k] * xa;
         }
     }
+#endif
+    ORC_OMP_FOR
     for (int64_t b = 0; b < nb; ++b)
         for (int i = 0; i < 6; ++i) {
             long double acc = 0.0L;
             for (int j = 0; j < 6; ++j) acc += (long double)W[36 * b + 6 * i + j] * F[6 * b + j];
             U[6 * b + i] = acc;
         }
+    ORC_OMP_FOR
     for (int64_t al = 0; al < nc; ++al) {
         int a = ia[al], b = ib[al];
         long double acc = 0.0L;
@@ -699,11 +739,14 @@ void orc_bbpgd(int64_t nb, int64_t nc, const int32_t *ia, const int32_t *ib, con
     int64_t k = 0;
     int conv = r <= tol;
     while (!conv && k < max_iter) {
+        ORC_OMP_FOR
         for (int64_t i = 0; i < nc; ++i) { double t = x[i] - alpha * g[i]; xn[i] = t > 0.0 ? t : 0.0; }
         orc_delassus_apply(nb, nc, ia, ib, nrm, ta, tb, W, s, xn, gn);
+        ORC_OMP_FOR
         for (int64_t i = 0; i < nc; ++i) gn[i] += q[i];
         long double ss = 0.0L, sy = 0.0L, yy = 0.0L;
         r = 0.0;
+        ORC_OMP_FOR_REDUCE
         for (int64_t i = 0; i < nc; ++i) {
             long double si = (long double)xn[i] - x[i], yi = (long double)gn[i] - g[i];
             ss += si * si; sy += si * yi; yy += yi * yi;

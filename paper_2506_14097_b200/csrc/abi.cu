@@ -127,12 +127,13 @@ __global__ void k_accept(int64_t nb, double bx, double by, double bz, const doub
 }
 
 // ------------------------------------------------------------ pair kernels
-// flag[k] = keep pair k; counts of degenerate / non-certified pairs and min phi.
+// flag[k] = keep pair k; counts of degenerate / non-certified pairs, min phi, and
+// the pairs inside the R14 guard band |Phi - thresh| < RELCP_GUARD_BAND.
 __global__ void __launch_bounds__(RELCP_NT) k_flag(int64_t np, const double *__restrict__ phi,
                                                    const int *__restrict__ stat, double thresh, int *__restrict__ flag,
                                                    double *part, unsigned *counter, double *out) {
-    __shared__ double sh[3 * 32];
-    double acc[3] = {0.0, 0.0, INFINITY};
+    __shared__ double sh[4 * 32];
+    double acc[4] = {0.0, 0.0, INFINITY, 0.0};
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < np; k += (int64_t)gridDim.x * blockDim.x) {
         const int s = stat[k];
         const double f = phi[k];
@@ -140,12 +141,15 @@ __global__ void __launch_bounds__(RELCP_NT) k_flag(int64_t np, const double *__r
         acc[0] += s == 1 ? 1.0 : 0.0;
         acc[1] += s == 2 ? 1.0 : 0.0;
         if (s != 1) acc[2] = fmin(acc[2], f);
+        // R14 guard band: a decision another correct fp64 code may take the other way
+        if (s != 1 && fabs(f - thresh) < RELCP_GUARD_BAND) acc[3] += 1.0;
     }
-    const int ops[3] = {0, 0, 2};
-    if (grid_reduce_last<3>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
+    const int ops[4] = {0, 0, 2, 0};
+    if (grid_reduce_last<4>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
         out[0] = acc[0];
         out[1] = acc[1];
         out[2] = acc[2];
+        out[3] = acc[3];
     }
 }
 
@@ -256,12 +260,13 @@ static int snsd_flag_scan(relcp_ctx *ctx, const double *pos, const int32_t *shap
     CK(cudaMemsetAsync(ctx->tflag.p + np, 0, sizeof(int), ctx->stream));
     int total = 0;
     CKS(scan_exclusive_int(ctx, ctx->tflag.p, off, np + 1, &total));  // syncs
-    CK(cudaMemcpyAsync(ctx->red_host, ctx->red.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->red_host, ctx->red.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     *nflag = total;
     *ndegen = (int64_t)ctx->red_host[0];
     *nnonconv = (int64_t)ctx->red_host[1];
     *minphi = ctx->red_host[2];
+    ctx->n_guard_total += (int64_t)ctx->red_host[3];
     PHASE(ctx, "snsd.flag_scan");
     return RELCP_OK;
 }
@@ -580,6 +585,7 @@ int relcp_step(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_const
     const int64_t nb = b->n;
     CKS(ensure_common(ctx, nb));
     PHASE(ctx, "step.enter");
+    const int64_t guard0 = ctx->n_guard_total;
     double t0 = now_ms();
     // W frozen at C^k; U_free (P:L557-561 / P:L522)
     CKS(op_build_W(ctx, b, ctx->W.p));
@@ -634,6 +640,7 @@ int relcp_step(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_const
     R.n_pairs = ctx->npairs;
     R.margin = ctx->margin;
     R.snsd_nonconv = ctx->snsd_nonconv_total;
+    R.n_guard = ctx->n_guard_total - guard0;
     // line 14: accept C^{k+1} = C_{n+1}, U^{k+1} = U_tot
     k_accept<<<grid_for(nb), RELCP_NT, 0, ctx->stream>>>(nb, ctx->p.box[0], ctx->p.box[1], ctx->p.box[2],
                                                          ctx->ptrial.p, ctx->qtrial.p, ctx->utot.p, b->pos, b->quat,
@@ -656,6 +663,7 @@ int relcp_get_stats(relcp_ctx *ctx, relcp_stats *out) {
     out->gather_ms = ctx->gather_ms;
     out->split_timed = ctx->split_timed;
     out->iter_ms = ctx->iter_ms;
+    out->n_guard = ctx->n_guard_total;
     return RELCP_OK;
 }
 
@@ -665,6 +673,7 @@ int relcp_reset_stats(relcp_ctx *ctx) {
     ctx->lcp_iterations = 0;
     ctx->iter_timed = ctx->split_timed = 0;
     ctx->scatter_ms = ctx->gather_ms = ctx->iter_ms = 0.0;
+    ctx->n_guard_total = 0;
     return RELCP_OK;
 }
 

@@ -29,6 +29,9 @@ inline void relcp_phase_mark(cudaStream_t st, const char *name) {
 #define RELCP_NT 256          // threads per block for streaming kernels
 #define RELCP_SM_COUNT 148    // B200
 #define RELCP_MAX_DIRS 1024   // cap on the SNSD start sample
+// R14 guard band: pairs with |Phi - threshold| below this are counted (n_guard):
+// two correct fp64 codes may decide them differently (R14)
+#define RELCP_GUARD_BAND 1e-10
 
 // ------------------------------------------------------------ device buffer
 template <class T>
@@ -85,6 +88,14 @@ struct LcpState {
     int n_ls;        // iterations whose full BB step the line search shortened
 };
 #define RELCP_GLL_M 10
+
+// power iteration step (finalize of k_gather's ||A v||^2): L = ||A v||, the next
+// input is scaled by 1/L
+__device__ __forceinline__ void power_finalize(LcpState *st, const double *acc) {
+    double nrm = sqrt(acc[0]);
+    st->L = nrm;
+    st->pnorm = nrm > 0.0 ? 1.0 / nrm : 0.0;
+}
 
 // Per-body mobility block W_b in a single 7-double form, stored as 7 SoA
 // planes W[k * nb + b]:
@@ -153,6 +164,7 @@ struct relcp_ctx {
     DevBuf<double> red;          // small reduction buffer
     double *red_host = nullptr;  // pinned (64 doubles)
     int64_t snsd_nonconv_total = 0;
+    int64_t n_guard_total = 0;   // R14 guard-band pairs since the last reset
 
     // counters / timing (relcp_get_stats)
     int64_t launches = 0;
@@ -208,7 +220,7 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
                const double *xscale_dev, double *U, double *F, const double *xb = nullptr,
                const double *gb = nullptr);
 int op_gather_apply(relcp_ctx *ctx, const relcp_constraints *cs, const double *U, double *y, double scale,
-                    int norm2);
+                    int norm2, double *acc_out = nullptr);
 // fused BB row pass (g_{k+1}, x_{k+2}, a-side sums Fa, BB reductions)
 int op_fused_rows(relcp_ctx *ctx, const relcp_constraints *cs, int64_t nb, double s, double *xA, double *xB);int op_row_dot_U(relcp_ctx *ctx, const relcp_constraints *cs, int64_t begin, int64_t end, const double *U,
                  double coef, double *out_add);
@@ -217,6 +229,23 @@ int store_merge_appended(relcp_ctx *ctx, relcp_constraints *cs, int64_t n_old, i
 int store_is_sorted_by_ia(relcp_ctx *ctx, const relcp_constraints *cs, int *sorted_host);
 // lcp.cu
 int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relcp_solve_report *rep);
+// split-reduction pieces of the BB solve for the domain-decomposed solve (dd.cu):
+// each writes its part's block-reduced partials to acc_out (device) instead of
+// finalizing; lcp_dd_finalize applies the finalize step of `kind` to ctx->st
+// from partials already combined over every part.
+enum { DD_POWER = 0, DD_INIT = 1, DD_ITER = 2, DD_FINISH = 3, DD_OBJECTIVE = 4 };
+int lcp_dd_nvals(int kind);                       // partials per kind
+const int *lcp_dd_ops(int kind);                  // 0 sum, 1 max per partial
+int lcp_dd_state_init(relcp_ctx *ctx, int64_t nc_global);
+int lcp_dd_project_fill(relcp_ctx *ctx, int64_t nc, double *lambda, double *v, double val);
+int lcp_dd_init(relcp_ctx *ctx, const relcp_constraints *cs, double s, double *acc_out);
+int lcp_dd_iter(relcp_ctx *ctx, const relcp_constraints *cs, double s, double *xB, double *gB, double *acc_out);
+int lcp_dd_finish(relcp_ctx *ctx, int64_t nc, double *x, double *g, const double *xo, const double *go,
+                  double *acc_out);
+int lcp_dd_objective(relcp_ctx *ctx, int64_t nc, const double *x, const double *g, const double *q,
+                     double *acc_out);
+int lcp_dd_finalize(relcp_ctx *ctx, int kind, const double *acc_dev);
+double lcp_scale(const relcp_ctx *ctx);
 // scan.cu
 int scan_exclusive_ll(relcp_ctx *ctx, const long long *in, long long *out, int64_t n, long long *total_host);
 int scan_exclusive_int(relcp_ctx *ctx, const int *in, int *out, int64_t n, int *total_host);

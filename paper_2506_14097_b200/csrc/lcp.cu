@@ -66,6 +66,28 @@ __global__ void k_state_init(LcpState *st, int64_t nc, double tol, long long max
     st->n_ls = 0;
 }
 
+// ---- finalize steps of the grid reductions (also applied by the domain-
+// decomposed solve, dd.cu, to partials combined over all parts)
+// acc = [max |min(x, g)|, nan flag, x^T (g + q)]
+__device__ void lcp_init_finalize(LcpState *st, const double *acc) {
+    double L = st->L > 0.0 && isfinite(st->L) ? st->L : 1.0;
+    st->L = L;
+    st->alpha = 1.0 / L;
+    st->resid = acc[0];
+    st->iter = 0;
+    st->f_cur = 0.5 * acc[2];
+    st->fhist[0] = st->f_cur;
+    if (acc[1] > 0.0) {
+        st->nan = 1;
+        st->done = 1;
+    } else if (acc[0] <= st->tol) {
+        st->conv = 1;
+        st->done = 1;
+    } else if (st->max_iter <= 0) {
+        st->done = 1;
+    }
+}
+
 // g = s D^T U + q for the (projected) warm start; r_0; alpha_0 = 1/L.
 template <bool CR>
 __global__ void __launch_bounds__(RELCP_NT) k_lcp_init(int64_t nc, int64_t cap, const int32_t *__restrict__ ia,
@@ -75,7 +97,7 @@ __global__ void __launch_bounds__(RELCP_NT) k_lcp_init(int64_t nc, int64_t cap, 
                                                        const double *__restrict__ U, double s,
                                                        const double *__restrict__ q, const double *__restrict__ x,
                                                        double *__restrict__ g, double *part, unsigned *counter,
-                                                       LcpState *st) {
+                                                       LcpState *st, double *acc_out) {
     __shared__ double sh[3 * 32];
     double acc[3] = {0.0, 0.0, 0.0};
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
@@ -88,23 +110,52 @@ __global__ void __launch_bounds__(RELCP_NT) k_lcp_init(int64_t nc, int64_t cap, 
     }
     const int ops[3] = {1, 1, 0};
     if (grid_reduce_last<3>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
-        double L = st->L > 0.0 && isfinite(st->L) ? st->L : 1.0;
-        st->L = L;
-        st->alpha = 1.0 / L;
-        st->resid = acc[0];
-        st->iter = 0;
-        st->f_cur = 0.5 * acc[2];
-        st->fhist[0] = st->f_cur;
-        if (acc[1] > 0.0) {
-            st->nan = 1;
-            st->done = 1;
-        } else if (acc[0] <= st->tol) {
-            st->conv = 1;
-            st->done = 1;
-        } else if (st->max_iter <= 0) {
-            st->done = 1;
+        if (acc_out) {  // domain decomposition: partials combined across parts first
+            for (int k = 0; k < 3; ++k) acc_out[k] = acc[k];
+            return;
         }
+        lcp_init_finalize(st, acc);
     }
+}
+
+// acc = [s.s, s.y, y.y, max |min(x+, g+)|, nan flag, g.d]: BB step, GLL line
+// search, convergence (see k_lcp_iter)
+__device__ void bb_iter_finalize(LcpState *st, const double *acc) {
+    const long long k = st->iter;
+    st->ss = acc[0];
+    st->sy = acc[1];
+    st->yy = acc[2];
+    st->resid = acc[3];
+    st->iter = k + 1;
+    if (acc[4] > 0.0 || !isfinite(acc[0]) || !isfinite(acc[1]) || !isfinite(acc[2]) || !isfinite(acc[5])) {
+        st->nan = 1;
+        st->done = 1;
+        return;
+    }
+    st->par ^= 1;  // (x+, g+) is the written slot
+    if (acc[3] <= st->tol) {  // the full step solves the LCP
+        st->fix = 0;
+        st->conv = 1;
+        st->done = 1;
+        return;
+    }
+    // nonmonotone line search along d = x+ - x (closed form, f quadratic)
+    const double gd = acc[5], dAd = acc[1];
+    double fmaxh = st->f_cur;
+#pragma unroll
+    for (int m = 0; m < RELCP_GLL_M; ++m) fmaxh = fmax(fmaxh, st->fhist[m]);
+    double t = 1.0;
+    if (!(st->f_cur + gd + 0.5 * dAd <= fmaxh + 1e-4 * gd) && dAd > 0.0) t = fmin(1.0, -gd / dAd);
+    st->f_cur += t * gd + 0.5 * t * t * dAd;
+    st->fhist[(k + 1) % RELCP_GLL_M] = st->f_cur;
+    st->fix = t < 1.0;
+    st->t_ls = t;
+    st->n_ls += t < 1.0;
+    // BB steps are invariant under the scaling s, y -> t s, t y
+    double al = (acc[1] <= 0.0 || acc[2] == 0.0) ? 1.0 / st->L : ((k % 2 == 0) ? acc[0] / acc[1] : acc[1] / acc[2]);
+    const double lo = 1e-10 / st->L, hi = 1e10 / st->L;
+    st->alpha = fmin(hi, fmax(lo, al));
+    if (k + 1 >= st->max_iter) st->done = 1;
 }
 
 // One BB projected-gradient update (the gather half of iteration k), with a
@@ -128,7 +179,7 @@ __global__ void __launch_bounds__(RELCP_NT, CR ? ITER_MINB_CR : ITER_MINB) k_lcp
                                                        const double *__restrict__ U, double s,
                                                        const double *__restrict__ q, double *xA, double *gA,
                                                        double *xB, double *gB, double *part, unsigned *counter,
-                                                       LcpState *st) {
+                                                       LcpState *st, double *acc_out) {
     __shared__ double sh[6 * 32];
     if (st->done) return;
     const double alpha = st->alpha;
@@ -185,49 +236,25 @@ __global__ void __launch_bounds__(RELCP_NT, CR ? ITER_MINB_CR : ITER_MINB) k_lcp
         pass(std::integral_constant<int, CR ? ITER_ILP_CR : ITER_ILP>{}, std::false_type{});
     const int ops[6] = {0, 0, 0, 1, 1, 0};
     if (grid_reduce_last<6>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
-        const long long k = st->iter;
-        st->ss = acc[0];
-        st->sy = acc[1];
-        st->yy = acc[2];
-        st->resid = acc[3];
-        st->iter = k + 1;
-        if (acc[4] > 0.0 || !isfinite(acc[0]) || !isfinite(acc[1]) || !isfinite(acc[2]) || !isfinite(acc[5])) {
-            st->nan = 1;
-            st->done = 1;
+        if (acc_out) {
+            for (int k = 0; k < 6; ++k) acc_out[k] = acc[k];
             return;
         }
-        st->par ^= 1;  // (x+, g+) is the written slot
-        if (acc[3] <= st->tol) {  // the full step solves the LCP
-            st->fix = 0;
-            st->conv = 1;
-            st->done = 1;
-            return;
-        }
-        // nonmonotone line search along d = x+ - x (closed form, f quadratic)
-        const double gd = acc[5], dAd = acc[1];
-        double fmaxh = st->f_cur;
-#pragma unroll
-        for (int m = 0; m < RELCP_GLL_M; ++m) fmaxh = fmax(fmaxh, st->fhist[m]);
-        double t = 1.0;
-        if (!(st->f_cur + gd + 0.5 * dAd <= fmaxh + 1e-4 * gd) && dAd > 0.0) t = fmin(1.0, -gd / dAd);
-        st->f_cur += t * gd + 0.5 * t * t * dAd;
-        st->fhist[(k + 1) % RELCP_GLL_M] = st->f_cur;
-        st->fix = t < 1.0;
-        st->t_ls = t;
-        st->n_ls += t < 1.0;
-        // BB steps are invariant under the scaling s, y -> t s, t y
-        double al = (acc[1] <= 0.0 || acc[2] == 0.0) ? 1.0 / st->L : ((k % 2 == 0) ? acc[0] / acc[1] : acc[1] / acc[2]);
-        const double lo = 1e-10 / st->L, hi = 1e10 / st->L;
-        st->alpha = fmin(hi, fmax(lo, al));
-        if (k + 1 >= st->max_iter) st->done = 1;
+        bb_iter_finalize(st, acc);
     }
+}
+
+__device__ void bb_finish_finalize(LcpState *st, const double *acc) {
+    st->resid = acc[0];
+    st->fix = 0;
+    st->conv = acc[0] <= st->tol;
 }
 
 // After a BB solve that ended on a shortened step (fix): the iterate is the
 // blend of the two slots; write it into (x, g) and recompute the residual.
 __global__ void __launch_bounds__(RELCP_NT) k_bb_finish(int64_t nc, double *x, double *g, const double *xo,
                                                         const double *go, double *part, unsigned *counter,
-                                                        LcpState *st) {
+                                                        LcpState *st, double *acc_out) {
     __shared__ double sh[32];
     const double tl = st->t_ls;
     double acc[1] = {0.0};
@@ -239,9 +266,11 @@ __global__ void __launch_bounds__(RELCP_NT) k_bb_finish(int64_t nc, double *x, d
     }
     const int ops[1] = {1};
     if (grid_reduce_last<1>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
-        st->resid = acc[0];
-        st->fix = 0;
-        st->conv = acc[0] <= st->tol;
+        if (acc_out) {
+            acc_out[0] = acc[0];
+            return;
+        }
+        bb_finish_finalize(st, acc);
     }
 }
 
@@ -318,13 +347,19 @@ __global__ void k_apgd_setup(LcpState *st) {
 // obj = x^T (g - q) = x^T A x
 __global__ void __launch_bounds__(RELCP_NT) k_objective(int64_t nc, const double *__restrict__ x,
                                                         const double *__restrict__ g, const double *__restrict__ q,
-                                                        double *part, unsigned *counter, LcpState *st) {
+                                                        double *part, unsigned *counter, LcpState *st,
+                                                        double *acc_out) {
     __shared__ double sh[32];
     double acc[1] = {0.0};
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x)
         acc[0] = fma(x[a], g[a] - q[a], acc[0]);
     const int ops[1] = {0};
-    if (grid_reduce_last<1>(acc, ops, part, counter, sh) && threadIdx.x == 0) st->obj = acc[0];
+    if (grid_reduce_last<1>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
+        if (acc_out)
+            acc_out[0] = acc[0];
+        else
+            st->obj = acc[0];
+    }
 }
 
 static double op_scale(const relcp_ctx *ctx) {
@@ -367,10 +402,10 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
 #define ROWS_ARGS nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->op_rs, ctx->rc.p
     if (cr)
         k_lcp_init<true><<<gridc, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g, ctx->partials.p,
-                                                     ctx->counter.p, ctx->st.p);
+                                                     ctx->counter.p, ctx->st.p, nullptr);
     else
         k_lcp_init<false><<<gridc, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g,
-                                                      ctx->partials.p, ctx->counter.p, ctx->st.p);
+                                                      ctx->partials.p, ctx->counter.p, ctx->st.p, nullptr);
     CKL();
     const bool apgd = ctx->p.solver == RELCP_SOLVER_APGD || (ctx->p.solver == RELCP_SOLVER_APGD_FUSED && !ctx->op_sorted);
     // fused APGD needs the sorted store (a-side rows contiguous); else plain APGD
@@ -447,10 +482,10 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
                                                                gB, ctx->partials.p, ctx->counter.p, ctx->st.p);
             else if (cr)
                 k_lcp_iter<true><<<gridi, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g, xB,
-                                                             gB, ctx->partials.p, ctx->counter.p, ctx->st.p);
+                                                             gB, ctx->partials.p, ctx->counter.p, ctx->st.p, nullptr);
             else
                 k_lcp_iter<false><<<gridi, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g, xB,
-                                                              gB, ctx->partials.p, ctx->counter.p, ctx->st.p);
+                                                              gB, ctx->partials.p, ctx->counter.p, ctx->st.p, nullptr);
             CKL();
             if (ev_on) CK(cudaEventRecord(ctx->ev[3 * j + 2], st));
         }
@@ -522,7 +557,7 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
         // current slot, x_k in the other one
         const bool pb = ctx->st_host->par != 0;
         k_bb_finish<<<gridc, RELCP_NT, 0, st>>>(nc, pb ? xB : cs->lambda, pb ? gB : cs->g, pb ? cs->lambda : xB,
-                                                pb ? cs->g : gB, ctx->partials.p, ctx->counter.p, ctx->st.p);
+                                                pb ? cs->g : gB, ctx->partials.p, ctx->counter.p, ctx->st.p, nullptr);
         CKL();
     }
     if (bb && ctx->st_host->par) {  // the current BB iterate lives in the second slot
@@ -535,7 +570,8 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
     }
     if (fused && ctx->st_host->par)  // the current fused-BB iterate lives in the second slot
         CK(cudaMemcpyAsync(cs->lambda, xB, sizeof(double) * nc, cudaMemcpyDeviceToDevice, st));
-    k_objective<<<gridc, RELCP_NT, 0, st>>>(nc, cs->lambda, cs->g, cs->q, ctx->partials.p, ctx->counter.p, ctx->st.p);
+    k_objective<<<gridc, RELCP_NT, 0, st>>>(nc, cs->lambda, cs->g, cs->q, ctx->partials.p, ctx->counter.p, ctx->st.p,
+                                            nullptr);
     CKL();
     CK(cudaMemcpyAsync(ctx->st_host, ctx->st.p, sizeof(LcpState), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -549,5 +585,90 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
     }
     if (h.nan) return set_err(ctx, RELCP_E_NAN, "solve: non-finite iterate after %lld iterations", h.iter);
     if (!h.conv) return RELCP_W_MAX_ITER;
+    return RELCP_OK;
+}
+
+
+// ------------------------------------------------------------ split reductions (dd.cu)
+static const int kDDops[5][6] = {{0}, {1, 1, 0}, {0, 0, 0, 1, 1, 0}, {1}, {0}};
+static const int kDDn[5] = {1, 3, 6, 1, 1};
+int lcp_dd_nvals(int kind) { return kDDn[kind]; }
+const int *lcp_dd_ops(int kind) { return kDDops[kind]; }
+double lcp_scale(const relcp_ctx *ctx) { return op_scale(ctx); }
+
+__global__ void k_dd_finalize(LcpState *st, int kind, const double *__restrict__ acc) {
+    double a[6];
+    for (int k = 0; k < 6; ++k) a[k] = k < 6 ? acc[k] : 0.0;
+    if (kind == DD_POWER) power_finalize(st, a);
+    else if (kind == DD_INIT) lcp_init_finalize(st, a);
+    else if (kind == DD_ITER) {
+        if (!st->done) bb_iter_finalize(st, a);
+    } else if (kind == DD_FINISH) bb_finish_finalize(st, a);
+    else st->obj = a[0];
+}
+
+int lcp_dd_state_init(relcp_ctx *ctx, int64_t nc_global) {
+    k_state_init<<<1, 1, 0, ctx->stream>>>(ctx->st.p, nc_global, ctx->p.lcp_tol, (long long)ctx->p.lcp_max_iter);
+    CKL();
+    return RELCP_OK;
+}
+
+int lcp_dd_project_fill(relcp_ctx *ctx, int64_t nc, double *lambda, double *v, double val) {
+    if (nc <= 0) return RELCP_OK;
+    k_project<<<grid_for(nc, RELCP_NT, ITER_MINB), RELCP_NT, 0, ctx->stream>>>(nc, lambda);
+    CKL();
+    k_fill<<<grid_for(nc, RELCP_NT, ITER_MINB), RELCP_NT, 0, ctx->stream>>>(nc, v, val);
+    CKL();
+    return RELCP_OK;
+}
+
+int lcp_dd_init(relcp_ctx *ctx, const relcp_constraints *cs, double s, double *acc_out) {
+    const int64_t nc = cs->count;
+    const int gridc = grid_for(nc, RELCP_NT, ITER_MINB);
+#define DD_ROWS nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->op_rs, ctx->rc.p
+    if (ctx->op_compact)
+        k_lcp_init<true><<<gridc, RELCP_NT, 0, ctx->stream>>>(DD_ROWS, ctx->U.p, s, cs->q, cs->lambda, cs->g,
+                                                              ctx->partials.p, ctx->counter.p, ctx->st.p, acc_out);
+    else
+        k_lcp_init<false><<<gridc, RELCP_NT, 0, ctx->stream>>>(DD_ROWS, ctx->U.p, s, cs->q, cs->lambda, cs->g,
+                                                               ctx->partials.p, ctx->counter.p, ctx->st.p, acc_out);
+    CKL();
+    return RELCP_OK;
+}
+
+int lcp_dd_iter(relcp_ctx *ctx, const relcp_constraints *cs, double s, double *xB, double *gB, double *acc_out) {
+    const int64_t nc = cs->count;
+    if (ctx->op_compact)
+        k_lcp_iter<true><<<grid_for(nc, RELCP_NT, ITER_MINB_CR), RELCP_NT, 0, ctx->stream>>>(
+            DD_ROWS, ctx->U.p, s, cs->q, cs->lambda, cs->g, xB, gB, ctx->partials.p, ctx->counter.p, ctx->st.p,
+            acc_out);
+    else
+        k_lcp_iter<false><<<grid_for(nc, RELCP_NT, ITER_MINB), RELCP_NT, 0, ctx->stream>>>(
+            DD_ROWS, ctx->U.p, s, cs->q, cs->lambda, cs->g, xB, gB, ctx->partials.p, ctx->counter.p, ctx->st.p,
+            acc_out);
+#undef DD_ROWS
+    CKL();
+    return RELCP_OK;
+}
+
+int lcp_dd_finish(relcp_ctx *ctx, int64_t nc, double *x, double *g, const double *xo, const double *go,
+                  double *acc_out) {
+    k_bb_finish<<<grid_for(nc, RELCP_NT, ITER_MINB), RELCP_NT, 0, ctx->stream>>>(nc, x, g, xo, go, ctx->partials.p,
+                                                                                ctx->counter.p, ctx->st.p, acc_out);
+    CKL();
+    return RELCP_OK;
+}
+
+int lcp_dd_objective(relcp_ctx *ctx, int64_t nc, const double *x, const double *g, const double *q,
+                     double *acc_out) {
+    k_objective<<<grid_for(nc, RELCP_NT, ITER_MINB), RELCP_NT, 0, ctx->stream>>>(nc, x, g, q, ctx->partials.p,
+                                                                                ctx->counter.p, ctx->st.p, acc_out);
+    CKL();
+    return RELCP_OK;
+}
+
+int lcp_dd_finalize(relcp_ctx *ctx, int kind, const double *acc_dev) {
+    k_dd_finalize<<<1, 1, 0, ctx->stream>>>(ctx->st.p, kind, acc_dev);
+    CKL();
     return RELCP_OK;
 }

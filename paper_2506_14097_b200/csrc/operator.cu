@@ -574,6 +574,7 @@ int op_fused_rows(relcp_ctx *ctx, const relcp_constraints *cs, int64_t nb, doubl
 #endif
 
 // y = scale * D^T U ; optionally the grid-wide ||y||^2 -> st->pnorm = 1/||y||, st->L = ||y||
+// (or, with acc_out, the block-reduced ||y||^2 of this part for dd.cu)
 // CR: rows from the compact planes rc (stride rs) instead of the store.
 template <bool CR>
 __global__ void __launch_bounds__(RELCP_NT, CR ? GATHER_MINB_CR : 4) k_gather(int64_t nc, int64_t cap, const int32_t *__restrict__ ia,
@@ -582,7 +583,7 @@ __global__ void __launch_bounds__(RELCP_NT, CR ? GATHER_MINB_CR : 4) k_gather(in
                                                      int64_t rs, const double *__restrict__ rc,
                                                      const double *__restrict__ U, double scale,
                                                      double *__restrict__ y, int norm2, double *part,
-                                                     unsigned *counter, LcpState *st) {
+                                                     unsigned *counter, LcpState *st, double *acc_out) {
     __shared__ double sh[32];
     double acc[1] = {0.0};
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -605,25 +606,27 @@ __global__ void __launch_bounds__(RELCP_NT, CR ? GATHER_MINB_CR : 4) k_gather(in
     if (!norm2) return;
     const int ops[1] = {0};
     if (grid_reduce_last<1>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
-        double nrm = sqrt(acc[0]);
-        st->L = nrm;
-        st->pnorm = nrm > 0.0 ? 1.0 / nrm : 0.0;
+        if (acc_out) {  // domain decomposition: combined over parts first (dd.cu)
+            acc_out[0] = acc[0];
+            return;
+        }
+        power_finalize(st, acc);
     }
 }
 
 int op_gather_apply(relcp_ctx *ctx, const relcp_constraints *cs, const double *U, double *y, double scale,
-                    int norm2) {
+                    int norm2, double *acc_out) {
     const int64_t nc = cs->count;
     if (nc == 0) return RELCP_OK;
     const int grid = grid_for(nc, RELCP_NT, ctx->op_compact ? GATHER_MINB_CR : 4);
     if (ctx->op_compact)
         k_gather<true><<<grid, RELCP_NT, 0, ctx->stream>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb,
                                                            ctx->op_rs, ctx->rc.p, U, scale, y, norm2, ctx->partials.p,
-                                                           ctx->counter.p, ctx->st.p);
+                                                           ctx->counter.p, ctx->st.p, acc_out);
     else
         k_gather<false><<<grid, RELCP_NT, 0, ctx->stream>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb,
                                                             ctx->op_rs, ctx->rc.p, U, scale, y, norm2, ctx->partials.p,
-                                                            ctx->counter.p, ctx->st.p);
+                                                            ctx->counter.p, ctx->st.p, acc_out);
     CKL();
     return RELCP_OK;
 }

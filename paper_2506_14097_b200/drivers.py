@@ -90,6 +90,38 @@ def snsd_vs_relcp(sc, capacity_per_body: int = 16, **kw):
     return out
 
 
+def relax(sc, dt: float = 1e-2, max_steps: int = 40, target: float | None = None, capacity_per_body: int = 16,
+          callback=None, **kw):
+    """Overdamped relaxation of a (possibly overlapping) scene to an
+    overlap-free state: ReLCP steps (Algorithm 1, overdamped form
+    P:L512-522, local drag P:L928-944) with zero velocity and no external
+    force until the accepted state's candidate scan has max overlap <= target
+    (default eps_NCP / 2, inside the stopping rule P:L645-648).  This is the
+    SURVEY §8(d) "-relaxed" companion construction (the theory assumes an
+    overlap-free start).  Returns (pos, quat, reports)."""
+    s = dict(sc)
+    s.update(dynamics=R.OVERDAMPED, dt=dt)
+    kw.setdefault("max_recursions", 50)
+    kw.setdefault("lcp_tol", 1e-8)
+    ctx = _ctx_for(s, **kw)
+    bodies = R.BodyState.from_scene(s)
+    bodies.vel.zero_()
+    cs = R.ConstraintStore(capacity_per_body * sc["n"] + 1024)
+    tgt = 0.5 * sc["eps_ncp"] if target is None else target
+    reps = []
+    for k in range(max_steps):
+        rep = ctx.step(bodies, cs)
+        rep.update(step=k)
+        reps.append(rep)
+        if callback:
+            callback(k, bodies, cs, rep)
+        if rep["status"] == 0 and rep["max_overlap"] <= tgt:
+            break
+    else:
+        raise RuntimeError(f"relax: max overlap {reps[-1]['max_overlap']:.3e} > {tgt:.1e} after {max_steps} steps")
+    return bodies.pos.clone(), bodies.quat.clone(), reps
+
+
 def box_length(phi0: float, L0: float, phi: float) -> float:
     """Cube edge at volume fraction phi for the same bodies (phi L^3 = const)."""
     return L0 * (phi0 / phi) ** (1.0 / 3.0)

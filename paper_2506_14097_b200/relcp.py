@@ -26,7 +26,10 @@ W_MAX_ITER, W_RECURSION_CAP, W_SNSD_NONCONV = 1, 2, 3
 EXPORTS = ["relcp_default_params", "relcp_create", "relcp_destroy", "relcp_last_error", "relcp_set_params",
            "relcp_generate_contacts", "relcp_prepare_operator", "relcp_delassus_apply", "relcp_wrench",
            "relcp_solve_lcp", "relcp_check_and_augment", "relcp_step", "relcp_get_pairs", "relcp_snsd_pairs",
-           "relcp_get_stats", "relcp_reset_stats", "relcp_set_timing", "relcp_load_constraints"]
+           "relcp_get_stats", "relcp_reset_stats", "relcp_set_timing", "relcp_load_constraints",
+           "relcp_dd_plan_host", "relcp_dd_nccl_unique_id", "relcp_dd_create", "relcp_dd_destroy",
+           "relcp_dd_last_error", "relcp_dd_load", "relcp_dd_info_get", "relcp_dd_delassus_apply", "relcp_dd_get_u",
+           "relcp_dd_solve_lcp"]
 
 P = ctypes.c_void_p
 i32, i64, f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
@@ -58,14 +61,14 @@ class SolveReport(ctypes.Structure):
 
 class Stats(ctypes.Structure):
     _fields_ = [("launches", i64), ("lcp_iterations", i64), ("iter_timed", i64), ("scatter_ms", f64),
-                ("gather_ms", f64), ("split_timed", i64), ("iter_ms", f64)]
+                ("gather_ms", f64), ("split_timed", i64), ("iter_ms", f64), ("n_guard", i64)]
 
 
 class StepReport(ctypes.Structure):
     _fields_ = [("recursions", i32), ("status", i32), ("n_pairs", i64), ("margin", f64), ("max_overlap", f64),
                 ("n_c", i64 * MAX_REC), ("lcp_iters", i64 * MAX_REC), ("residual", f64 * MAX_REC),
                 ("f_n", f64 * MAX_REC), ("ms_generate", f64), ("ms_solve", f64), ("ms_check", f64),
-                ("snsd_nonconv", i64)]
+                ("snsd_nonconv", i64), ("n_guard", i64)]
 
     def as_dict(self):
         r = self.recursions
@@ -73,7 +76,15 @@ class StepReport(ctypes.Structure):
                     max_overlap=self.max_overlap, n_c=list(self.n_c[:r + 1]),
                     iterations=list(self.lcp_iters[:r + 1]), residuals=list(self.residual[:r + 1]),
                     f=list(self.f_n[:r + 1]), ms_generate=self.ms_generate, ms_solve=self.ms_solve,
-                    ms_check=self.ms_check, snsd_nonconv=self.snsd_nonconv)
+                    ms_check=self.ms_check, snsd_nonconv=self.snsd_nonconv, n_guard=self.n_guard)
+
+
+class DDInfo(ctypes.Structure):
+    _fields_ = [("n_own", i64), ("n_ghost", i64), ("row_lo", i64), ("row_hi", i64), ("n_recv", i64),
+                ("n_boundary", i64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 _lib = None
@@ -118,8 +129,19 @@ def load(build_if_missing: bool = True):
     L.relcp_set_timing.argtypes = [P, i32]
     L.relcp_load_constraints.argtypes = [P, ctypes.POINTER(Bodies), ctypes.POINTER(Constraints), i64, P, P, P, P,
                                          P, P]
+    L.relcp_dd_plan_host.argtypes = [i32, P, i64, P, P, i32, ctypes.POINTER(DDInfo), P, P, P, P]
+    L.relcp_dd_nccl_unique_id.argtypes = [P]
+    L.relcp_dd_create.argtypes = [ctypes.POINTER(P), ctypes.POINTER(Params), P, i32, P, i32, P]
+    L.relcp_dd_destroy.argtypes = [P]
+    L.relcp_dd_last_error.argtypes = [P]
+    L.relcp_dd_last_error.restype = ctypes.c_char_p
+    L.relcp_dd_load.argtypes = [P, ctypes.POINTER(Bodies), ctypes.POINTER(Constraints)]
+    L.relcp_dd_info_get.argtypes = [P, i32, ctypes.POINTER(DDInfo)]
+    L.relcp_dd_delassus_apply.argtypes = [P, P, P, f64]
+    L.relcp_dd_get_u.argtypes = [P, P]
+    L.relcp_dd_solve_lcp.argtypes = [P, ctypes.POINTER(Constraints), ctypes.POINTER(SolveReport)]
     for name in EXPORTS:
-        if name not in ("relcp_default_params", "relcp_last_error"):
+        if name not in ("relcp_default_params", "relcp_last_error", "relcp_dd_last_error"):
             getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -365,7 +387,7 @@ class Context:
         self._check(self.L.relcp_get_stats(self.h, ctypes.byref(st)))
         return dict(launches=st.launches, lcp_iterations=st.lcp_iterations, iter_timed=st.iter_timed,
                     scatter_ms=st.scatter_ms, gather_ms=st.gather_ms, split_timed=st.split_timed,
-                    iter_ms=st.iter_ms)
+                    iter_ms=st.iter_ms, n_guard=st.n_guard)
 
     def reset_stats(self):
         self._check(self.L.relcp_reset_stats(self.h))
@@ -402,3 +424,100 @@ class Context:
                                             _ptr(st)))
         torch.cuda.synchronize()
         return phi[:m], nrm[:, :m], ra[:, :m], rb[:, :m], st[:m]
+
+
+# ---------------------------------------------------------------- domain decomposition
+def dd_plan_host(part_off, ia, ib, part: int):
+    """Host-only partition plan of `part` (relcp_dd_plan_host; no device):
+    info dict + ghost (global ids), gseg, rseg, recv_list (numpy)."""
+    L = load()
+    off = np.ascontiguousarray(part_off, dtype=np.int64)
+    ia = np.ascontiguousarray(ia, dtype=np.int32)
+    ib = np.ascontiguousarray(ib, dtype=np.int32)
+    K = len(off) - 1
+    info = DDInfo()
+    p = lambda a: a.ctypes.data_as(P) if a is not None and a.size else None
+    rc = L.relcp_dd_plan_host(K, p(off), len(ia), p(ia), p(ib), int(part), ctypes.byref(info), None, None, None, None)
+    if rc != OK:
+        raise RelcpError(rc, "relcp_dd_plan_host")
+    ghost = np.empty(info.n_ghost, dtype=np.int64)
+    gseg = np.empty(K + 1, dtype=np.int64)
+    rseg = np.empty(K + 1, dtype=np.int64)
+    recv = np.empty(info.n_recv, dtype=np.int32)
+    rc = L.relcp_dd_plan_host(K, p(off), len(ia), p(ia), p(ib), int(part), ctypes.byref(info), p(ghost), p(gseg),
+                              p(rseg), p(recv))
+    if rc != OK:
+        raise RelcpError(rc, "relcp_dd_plan_host")
+    return dict(info=info.as_dict(), ghost=ghost, gseg=gseg, rseg=rseg, recv_list=recv)
+
+
+def dd_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    rc = load().relcp_dd_nccl_unique_id(ctypes.cast(buf, P))
+    if rc != OK:
+        raise RelcpError(rc, "relcp_dd_nccl_unique_id")
+    return buf.raw
+
+
+class DomainDecomposition:
+    """relcp_dd: the Delassus operator / BB solve split over K body ranges.
+    rank < 0: all K parts here (VIRTUAL, one device); rank >= 0: this process
+    holds part `rank` of K (NCCL; nccl_uid from dd_nccl_unique_id on rank 0)."""
+
+    def __init__(self, part_off, rank: int = -1, nccl_uid: bytes | None = None, params: Params | None = None,
+                 stream: torch.cuda.Stream | None = None, **kw):
+        if not torch.cuda.is_available():
+            raise RuntimeError("relcp: no CUDA device (there is no CPU fallback)")
+        self.L = load()
+        self.params = params if params is not None else default_params(**kw)
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        self.off = np.ascontiguousarray(part_off, dtype=np.int64)
+        uid = ctypes.create_string_buffer(nccl_uid, 128) if nccl_uid is not None else None
+        h = P()
+        rc = self.L.relcp_dd_create(ctypes.byref(h), ctypes.byref(self.params), P(self.stream.cuda_stream),
+                                    len(self.off) - 1, self.off.ctypes.data_as(P), int(rank),
+                                    ctypes.cast(uid, P) if uid is not None else None)
+        if rc != OK:
+            raise RelcpError(rc, "relcp_dd_create failed")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.relcp_dd_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc < 0:
+            raise RelcpError(rc, self.L.relcp_dd_last_error(self.h).decode(errors="replace"))
+        return rc
+
+    def load(self, bodies: BodyState, cs: ConstraintStore):
+        self._views = (bodies.view(), cs.view())
+        self._check(self.L.relcp_dd_load(self.h, ctypes.byref(self._views[0]), ctypes.byref(self._views[1])))
+
+    def info(self, part: int):
+        inf = DDInfo()
+        self._check(self.L.relcp_dd_info_get(self.h, int(part), ctypes.byref(inf)))
+        return inf.as_dict()
+
+    def delassus_apply(self, x: torch.Tensor, y: torch.Tensor, scale: float = 1.0):
+        m = int(self._views[1].count)
+        self._check(self.L.relcp_dd_delassus_apply(self.h, _dptr(x, torch.float64, m, "x"),
+                                                   _dptr(y, torch.float64, m, "y"), float(scale)))
+
+    def get_U(self, U: torch.Tensor):
+        n = int(self._views[0].n)
+        self._check(self.L.relcp_dd_get_u(self.h, _dptr(U, torch.float64, 6 * n, "U")))
+
+    def solve_lcp(self, cs: ConstraintStore):
+        cv = cs.view()
+        rep = SolveReport()
+        rc = self._check(self.L.relcp_dd_solve_lcp(self.h, ctypes.byref(cv), ctypes.byref(rep)))
+        return dict(iterations=rep.iterations, residual=rep.residual, converged=bool(rep.converged),
+                    objective=rep.objective, L=rep.L, status=rc)

@@ -248,3 +248,17 @@ def test_bbpgd_vs_pgs_cfg1(orc):
     assert np.abs(F_p - F_b).max() <= 1e-6 * np.abs(F_b).max()
     assert np.abs(g_p - g_b).max() <= 1e-6 * np.abs(q).max()
     assert np.abs(x_p - x_b).max() <= 1e-6 * np.abs(x_b).max()
+
+
+def test_openmp_timing_build_same_apply(orc):
+    """bench.py's cpu_baseline times the OpenMP build of the same oracle
+    source (liboracle_omp.so): its Delassus apply is bitwise the serial one
+    (each thread adds its own bodies' wrench terms in the serial order)."""
+    from gen import scenes
+    b, ia, ib, n, ra, rb = scenes.local_constraint_network(3000, 9000, 3)
+    W = orc.body_W(b)
+    ta, tb = orc.rows(n, ra, rb)
+    x = np.random.default_rng(0).random(len(ia))
+    y1 = orc.delassus_apply(W, ia, ib, n, ta, tb, 1e-6, x)
+    y2 = orc.delassus_apply(W, ia, ib, n, ta, tb, 1e-6, x, openmp=True)
+    assert np.array_equal(y1, y2)
