@@ -57,7 +57,7 @@ N_FULL = 2_000_000
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_FULL)
@@ -146,7 +146,7 @@ def cpu_baseline_full(n, n_c):
                 sample=(f"oracle BB iterations (orc_bbpgd, long-double dots) at N={n} bodies, N_C={n_c} rows "
                         f"(cfg5-sized lattice-neighbour network from gen.scenes.local_constraint_network); "
                         f"{allc['iters']} iterations on {allc['threads']} threads (OpenMP build of the same "
-                        f"source, serial wrench scatter) and {one['iters']} on 1 thread; setup excluded"),
+                        f"source; each thread sums its own bodies' wrench terms) and {one['iters']} on 1 thread; setup excluded"),
                 cpu_model=cpu_model(), os_cpu_count=os.cpu_count(),
                 threads_1=dict(it_per_s=one["it_per_s"], apply_ms=one["apply_ms"], iterations=one["iters"]),
                 threads_all=dict(threads=allc["threads"], it_per_s=allc["it_per_s"], apply_ms=allc["apply_ms"],

@@ -163,6 +163,7 @@ struct DDPart {
     int k = 0;
     DDPlan plan;
     int64_t n_loc = 0;
+    bool empty = false;        // owns no body (hence no row, no ghost, no halo)
     relcp_ctx *ctx = nullptr;  // this part's operator (CSR, W, U, LCP state)
     DevBuf<int32_t> ia, ib;    // local ids of the owned rows
     DevBuf<double> quat, axes, inv_mass, inv_inertia;
@@ -349,6 +350,7 @@ static int dd_scatter(relcp_dd *dd, const double *x, const double *g, int mode, 
                       const double *gb) {
     DDCTX;
     for (DDPart *p : dd->parts) {
+        if (p->empty) continue;
         const int64_t r0 = p->plan.r_lo;
         CKS(op_scatter(p->ctx, p->n_loc, x + r0, g ? g + r0 : nullptr, mode, power ? &p->ctx->st.p->pnorm : nullptr,
                        p->ctx->U.p, p->F.p, xb ? xb + r0 : nullptr, gb ? gb + r0 : nullptr));
@@ -484,9 +486,10 @@ extern "C" int relcp_dd_load(relcp_dd *dd, const relcp_bodies *b, const relcp_co
         const DDPlan &pl = P->plan;
         const int64_t n_own = pl.hi - pl.lo, ng = (int64_t)pl.ghost.size(), m = pl.r_hi - pl.r_lo;
         P->n_loc = n_own + ng;
-        if (P->n_loc == 0) return set_err(ctx, RELCP_E_ARG, "dd_load: part %d has no bodies", k);
         int rc = relcp_create(&P->ctx, &ctx->p, ctx->stream);
         if (rc != RELCP_OK) return set_err(ctx, rc, "dd_load: part context");
+        P->empty = P->n_loc == 0;  // keeps its LCP state (reductions), no operator
+        if (P->empty) continue;
         const int64_t nl = P->n_loc;
         CK(P->gids.grow(nl)); CK(P->quat.grow(4 * nl)); CK(P->axes.grow(3 * nl)); CK(P->inv_mass.grow(nl));
         CK(P->inv_inertia.grow(3 * nl)); CK(P->kin.grow(nl)); CK(P->shape.grow(nl)); CK(P->F.grow(6 * nl));
@@ -587,7 +590,8 @@ extern "C" int relcp_dd_delassus_apply(relcp_dd *dd, const double *x, double *y,
     CKS(check_loaded(dd, nullptr));
     if (dd->nc > 0 && (!x || !y || x == y)) return set_err(ctx, RELCP_E_ARG, "dd apply: x, y required and distinct");
     CKS(dd_scatter(dd, x, nullptr, 0, false, nullptr, nullptr));
-    for (DDPart *p : dd->parts) CKS(op_gather_apply(p->ctx, &p->cs, p->ctx->U.p, y + p->plan.r_lo, scale, 0));
+    for (DDPart *p : dd->parts)
+        if (!p->empty) CKS(op_gather_apply(p->ctx, &p->cs, p->ctx->U.p, y + p->plan.r_lo, scale, 0));
     return RELCP_OK;
 }
 
@@ -641,12 +645,14 @@ extern "C" int relcp_dd_solve_lcp(relcp_dd *dd, relcp_constraints *cs, relcp_sol
         CKS(dd_scatter(dd, dd->vtmp.p, nullptr, 0, true, nullptr, nullptr));
         CKS(zero_acc());
         for (DDPart *p : dd->parts)
-            CKS(op_gather_apply(p->ctx, &p->cs, p->ctx->U.p, dd->vtmp.p + p->plan.r_lo, s, 1, acc_slot(dd, p)));
+            if (!p->empty)
+                CKS(op_gather_apply(p->ctx, &p->cs, p->ctx->U.p, dd->vtmp.p + p->plan.r_lo, s, 1, acc_slot(dd, p)));
         CKS(dd_reduce(dd, DD_POWER));
     }
     CKS(dd_scatter(dd, cs->lambda, nullptr, 0, false, nullptr, nullptr));
     CKS(zero_acc());
-    for (DDPart *p : dd->parts) CKS(lcp_dd_init(p->ctx, &p->cs, s, acc_slot(dd, p)));
+    for (DDPart *p : dd->parts)
+        if (!p->empty) CKS(lcp_dd_init(p->ctx, &p->cs, s, acc_slot(dd, p)));
     CKS(dd_reduce(dd, DD_INIT));
     const int batch = ctx->p.check_every > 0 ? ctx->p.check_every : 32;
     LcpState *h = dd->parts[0]->ctx->st_host;
@@ -661,7 +667,9 @@ extern "C" int relcp_dd_solve_lcp(relcp_dd *dd, relcp_constraints *cs, relcp_sol
             CKS(dd_scatter(dd, cs->lambda, cs->g, 1, false, dd->xB.p, dd->gB.p));
             CKS(zero_acc());
             for (DDPart *p : dd->parts)
-                CKS(lcp_dd_iter(p->ctx, &p->cs, s, dd->xB.p + p->plan.r_lo, dd->gB.p + p->plan.r_lo, acc_slot(dd, p)));
+                if (!p->empty)
+                    CKS(lcp_dd_iter(p->ctx, &p->cs, s, dd->xB.p + p->plan.r_lo, dd->gB.p + p->plan.r_lo,
+                                    acc_slot(dd, p)));
             CKS(dd_reduce(dd, DD_ITER));
         }
     }

@@ -511,7 +511,7 @@ class DomainDecomposition:
         self._check(self.L.relcp_dd_delassus_apply(self.h, _dptr(x, torch.float64, m, "x"),
                                                    _dptr(y, torch.float64, m, "y"), float(scale)))
 
-    def get_U(self, U: torch.Tensor):
+    def get_u(self, U: torch.Tensor):
         n = int(self._views[0].n)
         self._check(self.L.relcp_dd_get_u(self.h, _dptr(U, torch.float64, 6 * n, "U")))
 

@@ -339,7 +339,8 @@ def test_fullsize_cfg4_against_oracle_solution(R):
     assert rep["converged"] and rep["residual"] <= 1e-8
     lam = cs.lam[:cs.count].cpu().numpy()
     g = cs.g[:cs.count].cpu().numpy()
-    assert np.max(np.abs(g[ri] - g_r)) <= 1e-6 * head["g"]
+    # g is fixed only to the solvers' tolerance on active rows (|min(lambda, g)| <= tol on both sides, R2)
+    assert np.max(np.abs(g[ri] - g_r)) <= 1e-6 * head["g"] + 2 * head["tol"]
     assert np.max(np.abs(lam[ri] - lam_r)) <= 1e-6 * head["lam"]
     U = torch.empty(sc["n"], 6, dtype=torch.float64, device="cuda")
     ctx.prepare_operator(bodies, cs)

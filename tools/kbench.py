@@ -1,5 +1,5 @@
 """Kernel micro-bench / ncu target: cfg5 A_0 at N bodies; a few Delassus
-applies then a capped LCP solve.  python tools/kbench.py [N] [iters]"""
+applies then a capped LCP solve.  python tools/kbench.py [N] [iters] [final|relaxed]"""
 import os
 import sys
 import time
@@ -13,6 +13,11 @@ from paper_2506_14097_b200 import relcp as R  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 2_000_000
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 sc = scenes.cfg5(n=n)
+if len(sys.argv) > 3 and sys.argv[3] == "relaxed":
+    # the bench headline's store: cfg5 relaxed by the library (drivers.relax), A_0 at that state
+    from paper_2506_14097_b200 import drivers  # noqa: E402
+    pos, quat, _ = drivers.relax(sc, max_recursions=0, lcp_max_iter=20000, max_steps=60)
+    sc = scenes.with_state(sc, pos.cpu().numpy(), quat.cpu().numpy(), 55, "cfg5-relaxed")
 ctx = R.Context(dynamics=sc["dynamics"], dt=sc["dt"], box=list(sc["box"]), lcp_max_iter=iters, lcp_tol=1e-30,
                 solver=int(os.environ.get("RELCP_SOLVER", "0")))  # 20 power iterations: APGD steps 1/(1.1 L)
 bodies = R.BodyState.from_scene(sc)
