@@ -427,3 +427,19 @@ def local_constraint_network(n_bodies: int, n_con: int, seed: int, dynamics: int
     ra = rng.uniform(-0.7, 0.7, size=(n_con, 3))
     rb = rng.uniform(-0.7, 0.7, size=(n_con, 3))
     return b, ia, ib, nrm, ra, rb
+
+
+def relabelled(sc: dict, seed: int) -> dict:
+    """The same scene with its bodies relabelled by a seeded random permutation
+    (every per-body array permuted alike): the same physical problem, but body
+    indices no longer follow space (DESIGN.md §5 "Body order").  Relabelling
+    only; no per-body value changes."""
+    n = sc["n"]
+    perm = np.random.Generator(np.random.PCG64(seed)).permutation(n)
+    out = dict(sc)
+    for k, v in sc.items():
+        if isinstance(v, np.ndarray) and v.ndim >= 1 and v.shape[0] == n and k != "box":
+            out[k] = np.ascontiguousarray(v[perm])
+    out["name"] = f"{sc['name']}-relabelled{seed}"
+    out["relabel"] = perm
+    return out

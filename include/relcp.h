@@ -82,7 +82,15 @@ typedef struct relcp_params {
     double xi;            /* drag coefficient (overdamped) [1.0]          */
     int32_t n_dirs;       /* SNSD multistart sample size for overlaps [256] (R4)   */
     int32_t solver;       /* RELCP_SOLVER_BB [default] | RELCP_SOLVER_APGD         */
+    int32_t reorder;      /* relcp_step's internal body order: RELCP_REORDER_OFF,
+                             _AUTO [default: on from RELCP_REORDER_MIN_BODIES
+                             bodies], _ON (see relcp_step)                         */
 } relcp_params;
+
+#define RELCP_REORDER_OFF 0
+#define RELCP_REORDER_AUTO 1
+#define RELCP_REORDER_ON 2
+#define RELCP_REORDER_MIN_BODIES 65536
 
 /* LCP solvers (the paper names only the family; reading R1):
  *   BB   Barzilai-Borwein projected gradient (alternating BB1 / BB2 steps);
@@ -269,14 +277,25 @@ int relcp_check_and_augment(relcp_ctx *ctx, const relcp_bodies *Ck, relcp_constr
  * pos (wrapped into the periodic box), quat (normalised) and vel in place:
  * C^{k+1} = accepted trial configuration, U^{k+1} = U_free + sigma W D lambda.
  * `scratch` is the constraint store used for the step (its final content is
- * the step's A_c).  Warning W_RECURSION_CAP (the last trial configuration is
- * accepted and flagged). */
+ * the step's A_c, rows (ia < ib) sorted by (ia, ib, gen), R18).  Warning
+ * W_RECURSION_CAP (the last trial configuration is accepted and flagged).
+ * Internal body order (params.reorder): the step may run on a
+ * relabelled copy of the bodies in spatial cell order (cells ~ the mean
+ * spacing, row-major, ties by caller id) and of the store, so that the
+ * operator's gathers stay local whatever order the caller keeps its bodies in;
+ * labels are arbitrary, and the results are translated back (ids,
+ * rows re-oriented to ia < ib with n' = -n, t_a' = -t_b, t_b' = -t_a, sorted)
+ * before return.  Extra device memory: one more store of scratch->capacity
+ * rows and a copy of the body arrays.  After a reordered step, relcp_get_pairs
+ * returns the step's pairs in caller ids (i < j) in internal order and
+ * relcp_check_and_augment needs a new relcp_generate_contacts. */
 int relcp_step(relcp_ctx *ctx, relcp_bodies *inout, const double *f_ext, relcp_constraints *scratch,
                relcp_step_report *rep);
 
 /* Candidate pairs currently held by the context (after generate / augment):
  * *n_pairs = count; if pi/pj non-NULL (device, capacity cap) they receive the
- * pairs in (i, j) lexicographic order.  Synchronises. */
+ * pairs in (i, j) lexicographic order (after a reordered relcp_step: caller
+ * ids with i < j, in the internal order).  Synchronises. */
 int relcp_get_pairs(relcp_ctx *ctx, int32_t *pi, int32_t *pj, int64_t cap, int64_t *n_pairs);
 
 /* Counters kept by the context since creation / the last reset:

@@ -32,6 +32,7 @@ static int check_params(const relcp_params *p) {
     if (p->dynamics == RELCP_OVERDAMPED && !(p->xi > 0.0)) return 0;
     if (p->solver != RELCP_SOLVER_BB && p->solver != RELCP_SOLVER_APGD && p->solver != RELCP_SOLVER_APGD_FUSED)
         return 0;
+    if (p->reorder < RELCP_REORDER_OFF || p->reorder > RELCP_REORDER_ON) return 0;
     return 1;
 }
 
@@ -404,6 +405,7 @@ void relcp_default_params(relcp_params *p) {
     p->power_iters = 20;
     p->xi = 1.0;
     p->n_dirs = 256;
+    p->reorder = RELCP_REORDER_AUTO;
 }
 
 int relcp_create(relcp_ctx **out, const relcp_params *p, void *cuda_stream) {
@@ -447,7 +449,7 @@ int relcp_destroy(relcp_ctx *ctx) {
     if (!ctx) return RELCP_OK;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     ctx->W.release(); ctx->row_ptr.release(); ctx->deg.release(); ctx->fill.release();
-    ctx->ecid.release(); ctx->ew.release(); ctx->U.release(); ctx->F.release();
+    ctx->ecid.release(); ctx->ew.release(); ctx->jcid.release(); ctx->U.release(); ctx->F.release();
     ctx->partials.release(); ctx->counter.release(); ctx->st.release(); ctx->vtmp.release();
     ctx->pi.release(); ctx->pj.release(); ctx->Sig.release(); ctx->ufree.release(); ctx->utot.release();
     ctx->ptrial.release(); ctx->qtrial.release(); ctx->rad.release();
@@ -455,6 +457,10 @@ int relcp_destroy(relcp_ctx *ctx) {
     ctx->tflag.release(); ctx->tstat.release(); ctx->scan_ll.release(); ctx->scan_tmp.release();
     ctx->cell_count.release(); ctx->cell_start.release(); ctx->cell_fill.release(); ctx->cell_items.release();
     ctx->body_cell.release(); ctx->pair_cnt.release(); ctx->red.release();
+    ctx->ord_perm.release(); ctx->ord_inv.release(); ctx->ord_cell.release(); ctx->ord_cnt.release();
+    ctx->ord_start.release(); ctx->ord_key.release(); ctx->ob_pos.release(); ctx->ob_quat.release();
+    ctx->ob_axes.release(); ctx->ob_vel.release(); ctx->ob_im.release(); ctx->ob_ii.release(); ctx->ob_fext.release();
+    ctx->ob_kin.release(); ctx->ob_shape.release(); ctx->os_i.release(); ctx->os_d.release();
     if (ctx->ev_ready)
         for (int k = 0; k < 3 * 64 + 2; ++k) cudaEventDestroy(ctx->ev[k]);
     if (ctx->st_host) cudaFreeHost(ctx->st_host);
@@ -476,6 +482,7 @@ int relcp_set_params(relcp_ctx *ctx, const relcp_params *p) {
 
 int relcp_generate_contacts(relcp_ctx *ctx, const relcp_bodies *bodies, relcp_constraints *cs, int64_t *n_out) {
     CKS(check_views(ctx, bodies, cs));
+    ctx->pairs_internal = 0;
     const int64_t nb = bodies->n;
     CKS(ensure_common(ctx, nb));
     if (ctx->p.dynamics == RELCP_INERTIAL && !bodies->vel)
@@ -573,13 +580,16 @@ int relcp_solve_lcp(relcp_ctx *ctx, const relcp_bodies *bodies, relcp_constraint
 int relcp_check_and_augment(relcp_ctx *ctx, const relcp_bodies *Ck, relcp_constraints *cs, int32_t recursion,
                             int64_t *n_appended, double *min_phi) {
     CKS(check_views(ctx, Ck, cs));
+    if (ctx->pairs_internal) return set_err(ctx, RELCP_E_STATE, "check_and_augment: call relcp_generate_contacts first");
     return check_impl(ctx, Ck, cs, recursion, 1, n_appended, min_phi);
 }
 
-int relcp_step(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_constraints *cs, relcp_step_report *rep) {
-    CKS(check_views(ctx, b, cs));
-    if (!cs->g) return set_err(ctx, RELCP_E_ARG, "step: constraints.g is required");
-    if (ctx->p.dynamics == RELCP_INERTIAL && !b->vel) return set_err(ctx, RELCP_E_ARG, "step: inertial needs vel");
+}  // extern "C"
+
+// Algorithm 1 on one body labelling; relcp_step wraps it with the
+// internal body order (order.cu)
+static int step_core(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_constraints *cs,
+                     relcp_step_report *rep) {
     relcp_step_report R;
     memset(&R, 0, sizeof(R));
     const int64_t nb = b->n;
@@ -654,6 +664,37 @@ int relcp_step(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_const
     return warn > 0 ? warn : RELCP_OK;
 }
 
+extern "C" {
+
+int relcp_step(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_constraints *cs, relcp_step_report *rep) {
+    CKS(check_views(ctx, b, cs));
+    if (!cs->g) return set_err(ctx, RELCP_E_ARG, "step: constraints.g is required");
+    if (ctx->p.dynamics == RELCP_INERTIAL && !b->vel) return set_err(ctx, RELCP_E_ARG, "step: inertial needs vel");
+    const bool reorder = ctx->p.reorder == RELCP_REORDER_ON ||
+                         (ctx->p.reorder == RELCP_REORDER_AUTO && b->n >= RELCP_REORDER_MIN_BODIES);
+    ctx->pairs_internal = 0;
+    if (!reorder) return step_core(ctx, b, f_ext, cs, rep);
+    // internal cell order: relabel, run Algorithm 1, translate back (order.cu)
+    PHASE(ctx, "step.enter");
+    CKS(ord_body_perm(ctx, b->n, b->pos));
+    relcp_bodies bi;
+    const double *fi = nullptr;
+    CKS(ord_bodies_in(ctx, b, f_ext, &bi, &fi));
+    relcp_constraints ci;
+    CKS(ord_store(ctx, cs, &ci));
+    PHASE(ctx, "step.reorder_in");
+    const int rc = step_core(ctx, &bi, fi, &ci, rep);
+    ctx->pairs_internal = 1;
+    if (rc == RELCP_E_CAPACITY) cs->count = ci.count;
+    if (rc < 0) return rc;
+    CKS(ord_bodies_out(ctx, &bi, b));
+    CKS(ord_store_out(ctx, b->n, &ci, cs));
+    ctx->op_nc = -1;  // the operator was prepared on the internal store
+    CK(cudaStreamSynchronize(ctx->stream));
+    PHASE(ctx, "step.reorder_out");
+    return rc;
+}
+
 int relcp_get_stats(relcp_ctx *ctx, relcp_stats *out) {
     if (!ctx || !out) return RELCP_E_ARG;
     out->launches = ctx->launches;
@@ -688,7 +729,9 @@ int relcp_get_pairs(relcp_ctx *ctx, int32_t *pi, int32_t *pj, int64_t cap, int64
     if (n_pairs) *n_pairs = ctx->npairs;
     if (pi && pj) {
         int64_t m = ctx->npairs < cap ? ctx->npairs : cap;
-        if (m > 0) {
+        if (m > 0 && ctx->pairs_internal) {
+            CKS(ord_pairs_out(ctx, m, pi, pj));
+        } else if (m > 0) {
             CK(cudaMemcpyAsync(pi, ctx->pi.p, sizeof(int) * m, cudaMemcpyDeviceToDevice, ctx->stream));
             CK(cudaMemcpyAsync(pj, ctx->pj.p, sizeof(int) * m, cudaMemcpyDeviceToDevice, ctx->stream));
         }

@@ -119,6 +119,7 @@ struct relcp_ctx {
     int64_t op_rs = 0;               // compact row plane stride (= op_nc)
     DevBuf<double> rc;               // (6, op_nc) compact rows (rows.cuh), for the row passes
     int op_compact = 0;              // every row has t . n ~ 0: row passes read rc
+    int op_cb = 0;                   // K6's b-side payload is the compact (u, v, t_b,j1, t_b,j2)
     DevBuf<int> pa;                  // (nb + 1) a-side row pointer of a sorted store
     DevBuf<int> mi;                  // merge scratch (3, rows)
     DevBuf<double> md;               // merge scratch (13, rows)
@@ -126,8 +127,9 @@ struct relcp_ctx {
     DevBuf<int> row_ptr;     // (nb + 1)
     DevBuf<int> deg;         // (nb)  scratch
     DevBuf<int> fill;        // (nb)  scratch
-    DevBuf<int> ecid;        // (2 nc) constraint index of each half entry (body-major)
-    DevBuf<double> ew;       // (6, 2 nc) signed wrench payload, body-major
+    DevBuf<int> ecid;        // (E) CSR keys (side << 30 | constraint), body-major; build scratch
+    DevBuf<double> ew;       // (6 or 4, E) K6 payload, jagged-diagonal order (k_jds)
+    DevBuf<int> jcid;        // (E) constraint index of each entry, jagged-diagonal order
     DevBuf<double> U;        // (nb, 6) U = W D x of the last scatter
     DevBuf<double> F;        // (nb, 6) scratch for relcp_wrench
     DevBuf<double> partials; // (blocks, 4)
@@ -165,6 +167,14 @@ struct relcp_ctx {
     double *red_host = nullptr;  // pinned (64 doubles)
     int64_t snsd_nonconv_total = 0;
     int64_t n_guard_total = 0;   // R14 guard-band pairs since the last reset
+
+    // internal body order of relcp_step (order.cu)
+    DevBuf<int> ord_perm, ord_inv, ord_cell, ord_cnt, ord_start, ord_key;
+    DevBuf<double> ob_pos, ob_quat, ob_axes, ob_vel, ob_im, ob_ii, ob_fext;
+    DevBuf<int> ob_kin, ob_shape;
+    DevBuf<int> os_i;      // internal store ids (3, cap)
+    DevBuf<double> os_d;   // internal store values (13, cap)
+    int pairs_internal = 0;  // ctx->pi / pj hold internal ids (ord_perm maps them)
 
     // counters / timing (relcp_get_stats)
     int64_t launches = 0;
@@ -246,6 +256,14 @@ int lcp_dd_objective(relcp_ctx *ctx, int64_t nc, const double *x, const double *
                      double *acc_out);
 int lcp_dd_finalize(relcp_ctx *ctx, int kind, const double *acc_dev);
 double lcp_scale(const relcp_ctx *ctx);
+// order.cu (relcp_step's internal body order)
+int ord_body_perm(relcp_ctx *ctx, int64_t nb, const double *pos);
+int ord_bodies_in(relcp_ctx *ctx, const relcp_bodies *b, const double *f_ext, relcp_bodies *bi,
+                  const double **f_ext_i);
+int ord_bodies_out(relcp_ctx *ctx, const relcp_bodies *bi, relcp_bodies *b);
+int ord_store(relcp_ctx *ctx, const relcp_constraints *cs, relcp_constraints *ci);
+int ord_store_out(relcp_ctx *ctx, int64_t nb, const relcp_constraints *ci, relcp_constraints *cs);
+int ord_pairs_out(relcp_ctx *ctx, int64_t np, int32_t *oi, int32_t *oj);
 // scan.cu
 int scan_exclusive_ll(relcp_ctx *ctx, const long long *in, long long *out, int64_t n, long long *total_host);
 int scan_exclusive_int(relcp_ctx *ctx, const int *in, int *out, int64_t n, int *total_host);

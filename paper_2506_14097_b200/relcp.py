@@ -38,10 +38,11 @@ i32, i64, f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
 class Params(ctypes.Structure):
     _fields_ = [("dynamics", i32), ("max_recursions", i32), ("dt", f64), ("eps_ncp", f64), ("cutoff", f64),
                 ("lcp_tol", f64), ("lcp_max_iter", i64), ("check_every", i32), ("power_iters", i32),
-                ("box", f64 * 3), ("xi", f64), ("n_dirs", i32), ("solver", i32)]
+                ("box", f64 * 3), ("xi", f64), ("n_dirs", i32), ("solver", i32), ("reorder", i32)]
 
 
 SOLVER_BB, SOLVER_APGD, SOLVER_APGD_FUSED = 0, 1, 2
+REORDER_OFF, REORDER_AUTO, REORDER_ON = 0, 1, 2
 
 
 class Bodies(ctypes.Structure):

@@ -337,12 +337,13 @@ def _sorted_rows(ia, ib, gen):
     return np.lexsort((ib, ia, gen))
 
 
-def _compare_step(orc, R, sc, tol_cfg=1e-9, max_recursions=50, solver=0):
+def _compare_step(orc, R, sc, tol_cfg=1e-9, max_recursions=50, solver=0, reorder=1):
     # Both sides solve every LCP to r <= 1e-12: two independent solvers that
     # each stop at r <= 1e-10 leave rotations differing by ~1e-9 (measured
     # 1.4e-9 on cfg1), at the edge of the 1e-9 configuration tolerance.
     r = orc.relcp_step(sc, lcp_tol=1e-12, max_recursions=max_recursions)
-    ctx = _ctx(R, sc, lcp_tol=1e-12, max_recursions=max_recursions, lcp_max_iter=2_000_000, solver=solver)
+    ctx = _ctx(R, sc, lcp_tol=1e-12, max_recursions=max_recursions, lcp_max_iter=2_000_000, solver=solver,
+               reorder=reorder)
     bodies = R.BodyState.from_scene(sc)
     cs = R.ConstraintStore(8 * max(1, len(r["constraints"]["ia"])) + 64)
     rep = ctx.step(bodies, cs)
@@ -380,6 +381,49 @@ def test_step_parity_cfg1_apgd(orc, R, solver):
     """The whole step with APGD / fused APGD against the oracle's BB step
     (solution parity: every LCP solved to r <= 1e-12 on both sides)."""
     _compare_step(orc, R, scenes.cfg1(), solver=solver)
+
+
+@pytest.mark.parametrize("reorder", [0, 2])
+def test_step_parity_relabelled_cfg5_recipe(orc, R, reorder):
+    """Body-order independence: the cfg5 recipe at 1000 bodies
+    under a random relabelling, with the internal cell order off and forced
+    on.  The oracle steps the relabelled scene as given; the GPU store comes
+    back in the caller's labels, sorted, rows oriented ia < ib (R18)."""
+    sc = scenes.relabelled(scenes.suspension(1000, (1.0, 0.6, 0.4), 0.55, 5, dt=1e-3), 17)
+    r, rep, g = _compare_step(orc, R, sc, max_recursions=2, reorder=reorder)
+    assert np.all(g["ia"] < g["ib"])
+    key = g["ia"].astype(np.int64) * (1 << 40) + g["ib"].astype(np.int64) * 64 + g["gen"]
+    assert np.all(np.diff(key) > 0)
+
+
+def test_reorder_same_step(R):
+    """The internal order relabels, nothing else: the step of a relabelled
+    cfg5-recipe scene (3000 bodies) with reorder off and forced on gives the
+    same rows (ids, generations bit-exact; Phi, n, q to rounding), lambda to the
+    solver tolerance and the same accepted state."""
+    sc = scenes.relabelled(scenes.suspension(3000, (1.0, 0.6, 0.4), 0.55, 5, dt=1e-3), 23)
+    out = {}
+    for ro in (0, 2):
+        ctx = _ctx(R, sc, lcp_tol=1e-12, max_recursions=3, lcp_max_iter=2_000_000, reorder=ro)
+        bodies = R.BodyState.from_scene(sc)
+        cs = R.ConstraintStore(40000)
+        rep = ctx.step(bodies, cs)
+        pi, pj = ctx.get_pairs()
+        pairs = np.sort(pi.cpu().numpy().astype(np.int64) * sc["n"] + pj.cpu().numpy())
+        out[ro] = (rep, cs.to_numpy(), bodies.pos.cpu().numpy(), bodies.vel.cpu().numpy(), pairs)
+    (r0, c0, p0, v0, q0), (r2, c2, p2, v2, q2) = out[0], out[2]
+    assert r0["n_c"] == r2["n_c"] and r0["recursions"] == r2["recursions"]
+    assert np.array_equal(q0, q2)
+    for k in ("ia", "ib", "gen"):
+        assert np.array_equal(c0[k], c2[k])
+    assert np.max(np.abs(c0["phi"] - c2["phi"])) <= 1e-12
+    assert np.max(np.abs(c0["n"] - c2["n"])) <= 1e-10
+    lam = np.max(np.abs(c0["lam"]))
+    assert np.max(np.abs(c0["lam"] - c2["lam"])) <= 1e-6 * lam
+    d = p0 - p2
+    d -= sc["box"] * np.rint(d / sc["box"])
+    assert np.max(np.abs(d)) <= 1e-9
+    assert np.max(np.abs(v0 - v2)) <= 1e-6 * max(1.0, np.max(np.abs(v0)))
 
 
 def test_step_parity_overdamped_cfg2_recipe(orc, R):
