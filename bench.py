@@ -68,6 +68,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-apply", action="store_true")
     ap.add_argument("--no-literal", action="store_true", help="skip the capped literal-cfg5 secondary line")
+    ap.add_argument("--no-relabel", action="store_true", help="skip the relabelled-bodies secondary line")
     return ap.parse_args()
 
 
@@ -405,6 +406,28 @@ def run_ours(args, rank, world, dist):
         e2e = dict(value=eit / (ems / 1e3) * (world if dist else 1), unit=UNIT, h2d_bytes_per_step=int(h2d),
                    d2h_bytes_per_step=int(d2h), ms_per_step=ems / args.steps)
 
+    # ---- secondary: the same step with the bodies randomly relabelled (body
+    # indices no longer follow space), internal cell order on (the default at
+    # this size) and off (DESIGN.md §5 "Body order")
+    relabel = None
+    if not args.no_relabel:
+        scr = scenes.relabelled(sc, 99)
+        bodies_r = R.BodyState.from_scene(scr)
+        init_r = {k: getattr(bodies_r, k).clone() for k in ("pos", "quat", "vel")}
+        relabel = dict(note="cfg5-relaxed with a random body relabelling (PCG64(99) permutation)")
+        for lab, ro in (("reorder_on", R.REORDER_AUTO), ("reorder_off", R.REORDER_OFF)):
+            ctx_r = R.Context(dynamics=scr["dynamics"], dt=scr["dt"], box=list(scr["box"]), cutoff=scr["cutoff"],
+                              eps_ncp=scr["eps_ncp"], lcp_tol=1e-8, lcp_max_iter=args.lcp_max_iter,
+                              max_recursions=args.max_recursions, reorder=ro)
+            ms_r, st_r, rep_r, _ = time_steps(ctx_r, bodies_r, init_r, cs, args.steps, args.warmup, dist)
+            it_r, roof_r = roofline_of(st_r, rep_r, args.n, peak, ms_r)
+            ms_rm, it_ra = combine_ranks(ms_r, it_r, dist, dev)
+            relabel[lab] = dict(value=it_ra / (ms_rm / 1e3), unit=UNIT, ms_per_step=ms_rm / args.steps,
+                                iter_frac=roof_r["frac"], iter_ms=roof_r["iter_ms"],
+                                lcp_iters=rep_r[-1]["iterations"], n_c=rep_r[-1]["n_c"])
+            ctx_r.close()
+        del bodies_r, init_r
+
     # ---- secondary: the literal (overlapping) cfg5 start under the round-1 caps
     literal = None
     if not args.no_literal:
@@ -457,7 +480,7 @@ def run_ours(args, rank, world, dist):
         complete_step=complete,
         roofline=dict(bound="hbm", kernel="LCP iteration (K6 scatter + K7 gather)", unit="GB/s", traffic=traffic,
                       traffic_n_c=traffic_nc, traffic_over_algorithmic=traffic_ratio, peak_source=peak_src, **roof),
-        delassus_apply=apply, literal_cfg5=literal,
+        delassus_apply=apply, relabelled=relabel, literal_cfg5=literal,
         cpu_baseline=cpu, e2e=e2e, gpu_launches=stats["launches"], clocks=clk,
         step_report=step_report(last),
     )

@@ -83,14 +83,17 @@ typedef struct relcp_params {
     int32_t n_dirs;       /* SNSD multistart sample size for overlaps [256] (R4)   */
     int32_t solver;       /* RELCP_SOLVER_BB [default] | RELCP_SOLVER_APGD         */
     int32_t reorder;      /* relcp_step's internal body order: RELCP_REORDER_OFF,
-                             _AUTO [default: on from RELCP_REORDER_MIN_BODIES
-                             bodies], _ON (see relcp_step)                         */
+                             _AUTO [default: from RELCP_REORDER_MIN_BODIES bodies,
+                             when fewer than RELCP_REORDER_COHERENT of the
+                             consecutive caller bodies (b, b+1) lie in the same
+                             or adjacent cells], _ON (see relcp_step)              */
 } relcp_params;
 
 #define RELCP_REORDER_OFF 0
 #define RELCP_REORDER_AUTO 1
 #define RELCP_REORDER_ON 2
 #define RELCP_REORDER_MIN_BODIES 65536
+#define RELCP_REORDER_COHERENT 0.5
 
 /* LCP solvers (the paper names only the family; reading R1):
  *   BB   Barzilai-Borwein projected gradient (alternating BB1 / BB2 steps);

@@ -670,13 +670,16 @@ int relcp_step(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_const
     CKS(check_views(ctx, b, cs));
     if (!cs->g) return set_err(ctx, RELCP_E_ARG, "step: constraints.g is required");
     if (ctx->p.dynamics == RELCP_INERTIAL && !b->vel) return set_err(ctx, RELCP_E_ARG, "step: inertial needs vel");
-    const bool reorder = ctx->p.reorder == RELCP_REORDER_ON ||
-                         (ctx->p.reorder == RELCP_REORDER_AUTO && b->n >= RELCP_REORDER_MIN_BODIES);
+    const bool on = ctx->p.reorder == RELCP_REORDER_ON;
+    const bool maybe = ctx->p.reorder == RELCP_REORDER_AUTO && b->n >= RELCP_REORDER_MIN_BODIES;
     ctx->pairs_internal = 0;
-    if (!reorder) return step_core(ctx, b, f_ext, cs, rep);
-    // internal cell order: relabel, run Algorithm 1, translate back (order.cu)
+    if (!on && !maybe) return step_core(ctx, b, f_ext, cs, rep);
+    // internal cell order: relabel, run Algorithm 1, translate back (order.cu);
+    // AUTO keeps the caller's order when it already follows space
     PHASE(ctx, "step.enter");
-    CKS(ord_body_perm(ctx, b->n, b->pos));
+    double coh = 0.0;
+    CKS(ord_body_perm(ctx, b->n, b->pos, on ? nullptr : &coh));
+    if (!on && coh >= RELCP_REORDER_COHERENT) return step_core(ctx, b, f_ext, cs, rep);
     relcp_bodies bi;
     const double *fi = nullptr;
     CKS(ord_bodies_in(ctx, b, f_ext, &bi, &fi));

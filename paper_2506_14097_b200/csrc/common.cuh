@@ -257,7 +257,7 @@ int lcp_dd_objective(relcp_ctx *ctx, int64_t nc, const double *x, const double *
 int lcp_dd_finalize(relcp_ctx *ctx, int kind, const double *acc_dev);
 double lcp_scale(const relcp_ctx *ctx);
 // order.cu (relcp_step's internal body order)
-int ord_body_perm(relcp_ctx *ctx, int64_t nb, const double *pos);
+int ord_body_perm(relcp_ctx *ctx, int64_t nb, const double *pos, double *coherent);
 int ord_bodies_in(relcp_ctx *ctx, const relcp_bodies *b, const double *f_ext, relcp_bodies *bi,
                   const double **f_ext_i);
 int ord_bodies_out(relcp_ctx *ctx, const relcp_bodies *bi, relcp_bodies *b);

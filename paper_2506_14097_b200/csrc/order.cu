@@ -60,6 +60,22 @@ __global__ void k_ord_cell(int64_t nb, const double *__restrict__ pos, OrdGrid G
     }
 }
 
+// fraction of consecutive caller indices (b, b+1) in the same or adjacent cells
+__global__ void k_ord_coherence(int64_t nb, const int *__restrict__ cell, OrdGrid G, double *part, unsigned *counter,
+                                double *out) {
+    __shared__ double sh[32];
+    double v[1] = {0.0};
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b + 1 < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        const int c0 = cell[b], c1 = cell[b + 1];
+        const int dx = c0 % G.nc[0] - c1 % G.nc[0];
+        const int dy = (c0 / G.nc[0]) % G.nc[1] - (c1 / G.nc[0]) % G.nc[1];
+        const int dz = c0 / (G.nc[0] * G.nc[1]) - c1 / (G.nc[0] * G.nc[1]);
+        v[0] += (abs(dx) <= 1 && abs(dy) <= 1 && abs(dz) <= 1) ? 1.0 : 0.0;
+    }
+    const int ops[1] = {0};
+    if (grid_reduce_last<1>(v, ops, part, counter, sh) && threadIdx.x == 0) out[0] = v[0] / (double)(nb > 1 ? nb - 1 : 1);
+}
+
 __global__ void k_ord_fill(int64_t nb, const int *__restrict__ cell, const int *__restrict__ start,
                            int *__restrict__ fill, int *__restrict__ perm) {
     for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
@@ -89,7 +105,10 @@ __global__ void k_ord_inverse(int64_t nb, const int *__restrict__ perm, int *__r
         inv[perm[i]] = (int)i;
 }
 
-int ord_body_perm(relcp_ctx *ctx, int64_t nb, const double *pos) {
+// *coherent (if non-null) = fraction of consecutive caller bodies in the same
+// or adjacent cells; the permutation is built only when coherent is null or
+// below RELCP_REORDER_COHERENT (the caller's order already follows space)
+int ord_body_perm(relcp_ctx *ctx, int64_t nb, const double *pos, double *coherent) {
     cudaStream_t st = ctx->stream;
     CK(ctx->ord_perm.grow(nb));
     CK(ctx->ord_inv.grow(nb));
@@ -135,6 +154,15 @@ int ord_body_perm(relcp_ctx *ctx, int64_t nb, const double *pos) {
     CK(cudaMemsetAsync(ctx->ord_cnt.p, 0, sizeof(int) * (ncell + 1), st));
     k_ord_cell<<<grid_for(nb), RELCP_NT, 0, st>>>(nb, pos, G, ctx->ord_cell.p, ctx->ord_cnt.p);
     CKL();
+    if (coherent) {
+        k_ord_coherence<<<grid_for(nb), RELCP_NT, 0, st>>>(nb, ctx->ord_cell.p, G, ctx->partials.p, ctx->counter.p,
+                                                           ctx->red.p);
+        CKL();
+        CK(cudaMemcpyAsync(ctx->red_host, ctx->red.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        *coherent = ctx->red_host[0];
+        if (*coherent >= RELCP_REORDER_COHERENT) return RELCP_OK;
+    }
     CKS(scan_exclusive_int(ctx, ctx->ord_cnt.p, ctx->ord_start.p, ncell + 1, nullptr));
     CK(cudaMemsetAsync(ctx->ord_cnt.p, 0, sizeof(int) * (ncell + 1), st));
     k_ord_fill<<<grid_for(nb), RELCP_NT, 0, st>>>(nb, ctx->ord_cell.p, ctx->ord_start.p, ctx->ord_cnt.p,
