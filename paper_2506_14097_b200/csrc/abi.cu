@@ -449,7 +449,7 @@ int relcp_destroy(relcp_ctx *ctx) {
     if (!ctx) return RELCP_OK;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     ctx->W.release(); ctx->row_ptr.release(); ctx->deg.release(); ctx->fill.release();
-    ctx->ecid.release(); ctx->ew.release(); ctx->jcid.release(); ctx->U.release(); ctx->F.release();
+    ctx->ecid.release(); ctx->ew.release(); ctx->U.release(); ctx->F.release();
     ctx->partials.release(); ctx->counter.release(); ctx->st.release(); ctx->vtmp.release();
     ctx->pi.release(); ctx->pj.release(); ctx->Sig.release(); ctx->ufree.release(); ctx->utot.release();
     ctx->ptrial.release(); ctx->qtrial.release(); ctx->rad.release();

@@ -119,7 +119,6 @@ struct relcp_ctx {
     int64_t op_rs = 0;               // compact row plane stride (= op_nc)
     DevBuf<double> rc;               // (6, op_nc) compact rows (rows.cuh), for the row passes
     int op_compact = 0;              // every row has t . n ~ 0: row passes read rc
-    int op_cb = 0;                   // K6's b-side payload is the compact (u, v, t_b,j1, t_b,j2)
     DevBuf<int> pa;                  // (nb + 1) a-side row pointer of a sorted store
     DevBuf<int> mi;                  // merge scratch (3, rows)
     DevBuf<double> md;               // merge scratch (13, rows)
@@ -127,9 +126,8 @@ struct relcp_ctx {
     DevBuf<int> row_ptr;     // (nb + 1)
     DevBuf<int> deg;         // (nb)  scratch
     DevBuf<int> fill;        // (nb)  scratch
-    DevBuf<int> ecid;        // (E) CSR keys (side << 30 | constraint), body-major; build scratch
-    DevBuf<double> ew;       // (6 or 4, E) K6 payload, jagged-diagonal order (k_jds)
-    DevBuf<int> jcid;        // (E) constraint index of each entry, jagged-diagonal order
+    DevBuf<int> ecid;        // (2 nc) constraint index of each half entry (body-major)
+    DevBuf<double> ew;       // (6, 2 nc) signed wrench payload, body-major
     DevBuf<double> U;        // (nb, 6) U = W D x of the last scatter
     DevBuf<double> F;        // (nb, 6) scratch for relcp_wrench
     DevBuf<double> partials; // (blocks, 4)

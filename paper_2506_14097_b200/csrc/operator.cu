@@ -10,20 +10,16 @@
 //   * scatter U = W D x (K6) is a body-major pass.  One warp owns 32 bodies
 //     (one per lane).  With the library's sorted store (R18) the a-side rows
 //     of those bodies are one contiguous store range, read in place (n, t_a,
-//     x, g planes), streamed in coalesced 64-entry tiles into shared memory,
-//     and each lane sums its own body's rows in order.  The b-side entries
-//     come from a body-major CSR built once per operator (constraint id +
-//     payload) in JAGGED-DIAGONAL order within each 32-body warp block
-//     (k_jds): column j holds entry j of every lane that has one, so a lane
-//     reads its entries straight into registers with coalesced loads and no
-//     shared-memory staging; the payload is the compact (u, v, t_b,j1,
-//     t_b,j2) of the rows (32 B) when every row has t . n ~ 0, else the signed
-//     [n; t_b] (48 B).  An unsorted caller store puts both sides in the CSR.
-//     Fixed association (a-side rows, then CSR entries by constraint): bitwise
-//     deterministic, no atomics.  Then W_b (SoA planes) and a shared-memory
-//     transpose for a coalesced U_b store.  Its DRAM traffic is ~1.0x the
-//     §8(d) bytes; it is bound by load latency at the register-limited 32
-//     warps per SM (profiles/README.md lists the variants measured).
+//     x, g planes); the b-side entries come from a CSR (constraint id +
+//     signed [n; t_b] payload, built once per operator, sorted by constraint).
+//     An unsorted caller store puts both sides in the CSR.  Entries are
+//     streamed in coalesced 64-entry tiles into shared memory and each lane
+//     sums its own body's entries in order (fixed association: bitwise
+//     deterministic, no atomics), then applies W_b (SoA planes) and stores U_b
+//     through a shared-memory transpose (coalesced).  The kernel reaches 78 %
+//     of the copy bandwidth on its bytes and is limited by load latency (the
+//     dependent chains pa -> rows, row_ptr -> ecid -> x / g gathers); see
+//     profiles/README.md for the variants measured against it.
 //   * gather y = s D^T U (K7, k_gather) is a constraint-major streaming pass
 //     with U_a, U_b read from L2.  When every row has t . n ~ 0 (t = r x n),
 //     the row passes read a compact copy of the rows built here (k_compact,
@@ -44,9 +40,6 @@
 #endif
 #ifndef SCATTER_WAVES
 #define SCATTER_WAVES 8  // grid cap = 148 * SCATTER_MINB * waves (grid-stride over 32-body groups)
-#endif
-#ifndef K6_CB
-#define K6_CB 1  // sorted store with compact rows: compact b-side payload in K6 (jds_sum<true>)
 #endif
 #ifndef SCATTER_MINB
 #define SCATTER_MINB 8   // resident blocks per SM the register budget must allow (64 regs at 4 warps)
@@ -137,55 +130,21 @@ __global__ void k_sort_segments(int64_t nb, const int *__restrict__ row_ptr, int
     }
 }
 
-// Jagged-diagonal order of the body-major CSR, per warp block of 32
-// bodies: entry j of lane l's body goes to column j of the block, columns
-// stored one after the other, each holding the lanes whose body has more than
-// j entries, in lane order.  K6's lane l then finds its j-th entry at
-// base + sum_{j'<j} |column j'| + (rank of l in column j): every column is one
-// coalesced run, and the per-lane sums need no shared-memory staging.  The
-// per-body order (side, constraint) is the CSR's, so the sums associate
-// exactly as before.  Payload = signed [n; t] (-[n; t_a] a-side, +[n; t_b]
-// b-side), 6 planes.
-__global__ void k_jds(int64_t nb, const int *__restrict__ row_ptr, const int *__restrict__ ekey, int64_t cap,
-                      const double *__restrict__ n, const double *__restrict__ ta, const double *__restrict__ tb,
-                      int64_t E, int *__restrict__ jcid, double *__restrict__ ew, const double *__restrict__ rc,
-                      int64_t rs) {
-    const int lane = threadIdx.x & 31;
-    const unsigned lt = (1u << lane) - 1u;
-    const int64_t nwarp = (nb + 31) >> 5;
-    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nwarp;
-         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int64_t b = (w << 5) + lane;
-        const bool own = b < nb;
-        const int s = own ? row_ptr[b] : 0, d = own ? row_ptr[b + 1] - s : 0;
-        int off = __shfl_sync(0xffffffffu, s, 0);
-        const int maxd = __reduce_max_sync(0xffffffffu, (unsigned)d);
-        for (int j = 0; j < maxd; ++j) {
-            const unsigned m = __ballot_sync(0xffffffffu, d > j);
-            if (d > j) {
-                const int64_t pos = off + __popc(m & lt);
-                const int key = ekey[s + j];
-                const int64_t a = key & (EKEY_SIDE - 1);
-                const bool side_b = (key & EKEY_SIDE) != 0;
-                const double sg = side_b ? 1.0 : -1.0;
-                const double *t = side_b ? tb : ta;
-                jcid[pos] = (int)a;
-                if (rc) {  // compact b-side payload (u, v, t_b,j1, t_b,j2)
-                    ew[0 * E + pos] = rc[a];
-                    ew[1 * E + pos] = rc[rs + a];
-                    ew[2 * E + pos] = rc[4 * rs + a];
-                    ew[3 * E + pos] = rc[5 * rs + a];
-                } else {
-                    ew[0 * E + pos] = sg * n[a];
-                    ew[1 * E + pos] = sg * n[cap + a];
-                    ew[2 * E + pos] = sg * n[2 * cap + a];
-                    ew[3 * E + pos] = sg * t[a];
-                    ew[4 * E + pos] = sg * t[cap + a];
-                    ew[5 * E + pos] = sg * t[2 * cap + a];
-                }
-            }
-            off += __popc(m);
-        }
+__global__ void k_payload(int64_t E, int64_t cap, const double *__restrict__ n, const double *__restrict__ ta,
+                          const double *__restrict__ tb, int *ekey, double *__restrict__ ew) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+        const int key = ekey[e];
+        const int64_t a = key & (EKEY_SIDE - 1);
+        const bool side_b = (key & EKEY_SIDE) != 0;
+        const double sg = side_b ? 1.0 : -1.0;
+        const double *t = side_b ? tb : ta;
+        ew[0 * E + e] = sg * n[a];
+        ew[1 * E + e] = sg * n[cap + a];
+        ew[2 * E + e] = sg * n[2 * cap + a];
+        ew[3 * E + e] = sg * t[a];
+        ew[4 * E + e] = sg * t[cap + a];
+        ew[5 * E + e] = sg * t[2 * cap + a];
+        ekey[e] = (int)a;
     }
 }
 
@@ -233,7 +192,6 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
     CK(ctx->U.grow(6 * nb));
     CK(ctx->ecid.grow(E > 0 ? E : 1));
     CK(ctx->ew.grow(6 * (E > 0 ? E : 1)));
-    CK(ctx->jcid.grow(E > 0 ? E : 1));
     CK(ctx->pa.grow(nb + 1));
     CK(ctx->rc.grow(6 * (nc > 0 ? nc : 1)));
     CKS(op_build_W(ctx, b, ctx->W.p));
@@ -243,8 +201,8 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
     CK(cudaMemsetAsync(ctx->pa.p, 0, sizeof(int) * (nb + 1), ctx->stream));
     CK(cudaMemsetAsync(ctx->fill.p, 0, sizeof(int) * (nb + 2), ctx->stream));  // fill[nb] bad, [nb+1] non-orthogonal
     if (nc > 0) {
-        k_degree<<<grid_for(nc), RELCP_NT, 0, ctx->stream>>>(
-            nc, cs->ia, cs->ib, sorted ? ctx->pa.p : ctx->deg.p, ctx->deg.p, nb, ctx->fill.p + nb);
+        k_degree<<<grid_for(nc), RELCP_NT, 0, ctx->stream>>>(nc, cs->ia, cs->ib, sorted ? ctx->pa.p : ctx->deg.p,
+                                                             ctx->deg.p, nb, ctx->fill.p + nb);
         CKL();
         k_compact<<<grid_for(nc), RELCP_NT, 0, ctx->stream>>>(nc, cs->capacity, cs->n, cs->ta, cs->tb, nc, ctx->rc.p,
                                                               ctx->fill.p + nb + 1);
@@ -258,7 +216,6 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
     CK(cudaStreamSynchronize(ctx->stream));
     if (flags[0]) return set_err(ctx, RELCP_E_ARG, "prepare: body index out of range or ia == ib");
     ctx->op_compact = nc > 0 && !flags[1];
-    ctx->op_cb = K6_CB && sorted && ctx->op_compact;
     const int64_t Ee = sorted ? nc : E;  // CSR entries: b-side only when sorted
     if (nc > 0) {
         CK(cudaMemsetAsync(ctx->fill.p, 0, sizeof(int) * nb, ctx->stream));
@@ -267,9 +224,8 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
         CKL();
         k_sort_segments<<<grid_for(nb, 128), 128, 0, ctx->stream>>>(nb, ctx->row_ptr.p, ctx->ecid.p);
         CKL();
-        k_jds<<<grid_for(32 * ((nb + 31) / 32)), RELCP_NT, 0, ctx->stream>>>(
-            nb, ctx->row_ptr.p, ctx->ecid.p, cs->capacity, cs->n, cs->ta, cs->tb, Ee, ctx->jcid.p, ctx->ew.p,
-            ctx->op_cb ? ctx->rc.p : nullptr, nc);
+        k_payload<<<grid_for(Ee), RELCP_NT, 0, ctx->stream>>>(Ee, cs->capacity, cs->n, cs->ta, cs->tb, ctx->ecid.p,
+                                                              ctx->ew.p);
         CKL();
     }
     ctx->op_sorted = sorted;
@@ -289,8 +245,8 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
 //
 // SORTED (store sorted by ia, the library's own order, R18): body b's a-side
 // rows are the store rows [pa[b], pa[b+1]) and contribute -[n; t_a] x_eff read
-// straight from the store planes; row_ptr / jcid / ew then hold only the
-// b-side entries (+[n; t_b]).  Otherwise row_ptr / jcid / ew hold both sides.
+// straight from the store planes; row_ptr / ecid / ew then hold only the
+// b-side entries (+[n; t_b]).  Otherwise row_ptr / ecid / ew hold both sides.
 // Per-body order: a-side rows, then CSR entries -- fixed, deterministic.
 struct V6 {
     double v[6];
@@ -298,67 +254,12 @@ struct V6 {
 // the U / F transpose reuses a warp's staging area: 2 x 32 x 6 doubles
 static_assert(3 * (SCATTER_TILE + 1) * 2 >= 2 * 192, "SCATTER_TILE too small for the U/F staging");
 
-// Lane sum over its body's jagged-diagonal CSR entries (k_jds): entry j at
-// off + sum_{j'<j} |column j'| + rank of the lane in column j.  Each column is
-// one coalesced run of (constraint id, 6 payload planes); x_eff is gathered by
-// id.  The lane adds its entries in CSR order (fixed association) straight
-// into registers: no shared-memory staging (the staged tiles' writes and
-// data-dependent per-lane reads were about half of K6's L1 wavefronts).
-// CB (sorted store with compact rows, b-side only): the payload is the row's
-// compact (u, v, t_b,j1, t_b,j2) (rows.cuh), 32 instead of 48 bytes per entry,
-// decoded in registers (the operator's b-side half then equals the compact
-// rows K7 applies).
-template <bool CB, class XE>
-__device__ __forceinline__ void jds_sum(int d, int off, int c_next, const int *__restrict__ jcid,
-                                        const double *__restrict__ ew, int64_t E, XE &&xeff, double f[6]) {
-    // c_next: the lane's column-0 id, loaded by the caller before its a-side
-    // work; each trip loads the next column's id, so the x_eff gathers and the
-    // payload loads of a column are one latency, not two
-    const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
-    const int maxd = (int)__reduce_max_sync(0xffffffffu, (unsigned)d);
-    unsigned m = __ballot_sync(0xffffffffu, d > 0);
-    for (int j = 0; j < maxd; ++j) {
-        const int c = c_next;
-        const int64_t p = off + __popc(m & lt);
-        const unsigned m1 = __ballot_sync(0xffffffffu, d > j + 1);
-        if (d > j + 1) c_next = jcid[off + __popc(m) + __popc(m1 & lt)];
-        if (d > j) {
-            double w[6];
-            if (CB) {
-                const double u = ew[p], v = ew[E + p], b1 = ew[2 * E + p], b2 = ew[3 * E + p];
-                const double xv = xeff(c);
-                const CNormal cn = cn_decode(u, v);
-                double t[3];
-                t_expand(cn, b1, b2, t);
-                w[0] = cn.n[0]; w[1] = cn.n[1]; w[2] = cn.n[2];
-                w[3] = t[0]; w[4] = t[1]; w[5] = t[2];
-#pragma unroll
-                for (int k = 0; k < 6; ++k) f[k] += w[k] * xv;
-            } else {
-#pragma unroll
-                for (int k = 0; k < 6; ++k) w[k] = ew[k * E + p];
-                const double xv = xeff(c);
-#pragma unroll
-                for (int k = 0; k < 6; ++k) f[k] += w[k] * xv;
-            }
-        }
-        off += __popc(m);
-        m = m1;
-    }
-}
-
-// id of the lane's column-0 entry (jds_sum's first prefetch)
-__device__ __forceinline__ int jds_first(int d, int off, const int *__restrict__ jcid) {
-    const unsigned m = __ballot_sync(0xffffffffu, d > 0);
-    return d > 0 ? jcid[off + __popc(m & ((1u << (threadIdx.x & 31)) - 1u))] : 0;
-}
-
 // MODE: 0 apply (x_eff = x), 1 BB step (x_eff = max(0, x - alpha g)),
 // 2 APGD step (y = x + beta (x - x'), g_y likewise, x_eff = max(0, y - t g_y);
 // (x, g) / (x', g') are (x, g) / (xb, gb) or swapped by the device parity bit).
-template <int MODE, bool SORTED, bool CB>
+template <int MODE, bool SORTED>
 __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
-    int64_t nb, int64_t E, const int *__restrict__ row_ptr, const int *__restrict__ jcid,
+    int64_t nb, int64_t E, const int *__restrict__ row_ptr, const int *__restrict__ ecid,
     const double *__restrict__ ew, const int *__restrict__ pa, int64_t cap, const double *__restrict__ cn,
     const double *__restrict__ cta, const double *__restrict__ x, const double *__restrict__ g,
     const double *__restrict__ xb, const double *__restrict__ gb, const LcpState *__restrict__ st,
@@ -449,11 +350,6 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
                 __syncwarp();
             }
         };
-        // b-side (all entries for an unsorted store): jagged-diagonal CSR; its
-        // first ids are loaded before the a-side tiles so they arrive meanwhile
-        const int sb = own ? row_ptr[b] : 0, db = own ? row_ptr[b + 1] - sb : 0;
-        const int offb = __shfl_sync(0xffffffffu, sb, 0);
-        const int c0 = jds_first(db, offb, jcid);
         if (MODE == 3) {
             // a-side sums were formed by the fused row pass (k_fused_rows)
             if (own)
@@ -472,7 +368,14 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
                 return v;
             });
         }
-        jds_sum<CB>(db, offb, c0, jcid, ew, E, xeff, f);
+        const int s = own ? row_ptr[b] : 0, t = own ? row_ptr[b + 1] : 0;
+        tiles(s, t, [&](int e) {
+            const double xv = xeff(ecid[e]);
+            V6 v;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) v.v[k] = ew[k * E + e] * xv;
+            return v;
+        });
         // U_b = W_b F_b ; staged through shared memory for a coalesced AoS store
         double u[6] = {0, 0, 0, 0, 0, 0};
         if (own) {
@@ -517,21 +420,20 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
     const int *pa = ctx->pa.p;
     const int64_t cap = ctx->op_cap;
     const double *cn = ctx->op_n, *cta = ctx->op_ta;
-#define SCATTER_ARGS nb, E, ctx->row_ptr.p, ctx->jcid.p, ctx->ew.p, pa, cap, cn, cta, x, g, xb, gb, ctx->st.p, \
+#define SCATTER_ARGS nb, E, ctx->row_ptr.p, ctx->ecid.p, ctx->ew.p, pa, cap, cn, cta, x, g, xb, gb, ctx->st.p, \
                      xscale_dev, ctx->W.p, U, F, ctx->Fa.p
-    if (mode == 3 && !ctx->op_sorted) return set_err(ctx, RELCP_E_STATE, "fused solver needs a store sorted by ia");
-    const bool cb = ctx->op_sorted && ctx->op_cb;
-#define K6_LAUNCH(S, C)                                                                           \
-    do {                                                                                          \
-        if (mode == 1) k_scatter<1, S, C><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);                \
-        else if (mode == 2) k_scatter<2, S, C><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);           \
-        else if (mode == 3) k_scatter<3, S, C><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);           \
-        else k_scatter<0, S, C><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);                          \
-    } while (0)
-    if (cb) K6_LAUNCH(true, true);
-    else if (ctx->op_sorted) K6_LAUNCH(true, false);
-    else K6_LAUNCH(false, false);
-#undef K6_LAUNCH
+    if (mode == 3) {
+        if (!ctx->op_sorted) return set_err(ctx, RELCP_E_STATE, "fused solver needs a store sorted by ia");
+        k_scatter<3, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+    } else if (ctx->op_sorted) {
+        if (mode == 1) k_scatter<1, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+        else if (mode == 2) k_scatter<2, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+        else k_scatter<0, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+    } else {
+        if (mode == 1) k_scatter<1, false><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+        else if (mode == 2) k_scatter<2, false><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+        else k_scatter<0, false><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+    }
 #undef SCATTER_ARGS
     CKL();
     return RELCP_OK;
