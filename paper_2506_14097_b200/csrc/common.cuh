@@ -156,6 +156,7 @@ struct relcp_ctx {
     DevBuf<int> multi;          // pairs needing the SNSD multistart (stage 2)
     DevBuf<int> nlist;          // ellipsoid pairs under the SNSD bound (Newton stage 1)
     DevBuf<double> dirs;        // (3, dirs_n) multistart directions (k_dirs)
+    DevBuf<float> dirs32;       // the same, fp32 (stage-2 screening)
     int dirs_n = 0;
     DevBuf<long long> scan_ll;  // scan scratch
     DevBuf<long long> scan_tmp;

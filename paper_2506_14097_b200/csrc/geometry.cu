@@ -287,7 +287,7 @@ __device__ int snsd_stage1(const double *d, const Sym &Sa, const Sym &Sb, double
 // The n_dirs-point Fibonacci sphere of the stage-2 multistart, (3, n_dirs)
 // planes: m_i = (r cos(g i), r sin(g i), z), z = 1 - (2i + 1)/n, r = sqrt(1 - z^2),
 // g = pi (3 - sqrt 5).  Shared by every pair, so tabulated once per context.
-__global__ void k_dirs(int n_dirs, double *__restrict__ dirs) {
+__global__ void k_dirs(int n_dirs, double *__restrict__ dirs, float *__restrict__ dirs32) {
     const double ga = 3.14159265358979323846 * (3.0 - sqrt(5.0));
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_dirs; i += gridDim.x * blockDim.x) {
         const double z = 1.0 - (2.0 * i + 1.0) / n_dirs;
@@ -297,7 +297,28 @@ __global__ void k_dirs(int n_dirs, double *__restrict__ dirs) {
         dirs[i] = r * cs;
         dirs[n_dirs + i] = r * sn;
         dirs[2 * n_dirs + i] = z;
+        dirs32[i] = (float)(r * cs);
+        dirs32[n_dirs + i] = (float)(r * sn);
+        dirs32[2 * n_dirs + i] = (float)z;
     }
+}
+
+// fp32 value of F at a sample direction: the stage-2 screening only RANKS the
+// samples to pick the Newton starts (refined in fp64 from the fp64 table), so
+// single precision is enough there and runs on the fp32 pipe / MUFU
+struct Sym32 {
+    float xx, xy, xz, yy, yz, zz;
+};
+__device__ __forceinline__ Sym32 sym32(const Sym &S) {
+    return Sym32{(float)S.xx, (float)S.xy, (float)S.xz, (float)S.yy, (float)S.yz, (float)S.zz};
+}
+__device__ __forceinline__ float fval32(const float *n, const float *d, const Sym32 &A, const Sym32 &B) {
+    const float ta0 = A.xx * n[0] + A.xy * n[1] + A.xz * n[2], ta1 = A.xy * n[0] + A.yy * n[1] + A.yz * n[2],
+                ta2 = A.xz * n[0] + A.yz * n[1] + A.zz * n[2];
+    const float tb0 = B.xx * n[0] + B.xy * n[1] + B.xz * n[2], tb1 = B.xy * n[0] + B.yy * n[1] + B.yz * n[2],
+                tb2 = B.xz * n[0] + B.yz * n[1] + B.zz * n[2];
+    return n[0] * d[0] + n[1] * d[1] + n[2] * d[2] - sqrtf(n[0] * ta0 + n[1] * ta1 + n[2] * ta2) -
+           sqrtf(n[0] * tb0 + n[1] * tb1 + n[2] * tb2);
 }
 
 // Stage 2 (overlap / touching): multistart from `n_dirs`-sample directions in
@@ -307,8 +328,8 @@ __global__ void k_dirs(int n_dirs, double *__restrict__ dirs) {
 #define SNSD_SEP_COS 0.9  // ~26 deg
 #endif
 __device__ int snsd_stage2(const double *d, const Sym &Sa, const Sym &Sb, int n_dirs,
-                           const double *__restrict__ dirs, double *nb, int st_best, double &phi, double *nout,
-                           double *ra, double *rb) {
+                           const double *__restrict__ dirs, const float *__restrict__ dirs32, double *nb,
+                           int st_best, double &phi, double *nout, double *ra, double *rb) {
     const double dn = sqrt(d3(d, d));
     const double dh[3] = {d[0] / dn, d[1] / dn, d[2] / dn};
     Eval Eb;
@@ -323,14 +344,16 @@ __device__ int snsd_stage2(const double *d, const Sym &Sa, const Sym &Sb, int n_
         // (Leaders hold sample indices; their directions are re-read from the
         // table, which stays in L1.)  Ties keep the earlier sample.
         constexpr int K = 4;
-        double topf[K];
+        float topf[K];
         int topi[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) { topf[k] = -INFINITY; topi[k] = -1; }
+        const float d32[3] = {(float)d[0], (float)d[1], (float)d[2]};
+        const Sym32 A32 = sym32(Sa), B32 = sym32(Sb);
         for (int i = 0; i < n_dirs; ++i) {
             // warp-uniform address: one broadcast load per plane
-            const double m[3] = {__ldg(dirs + i), __ldg(dirs + n_dirs + i), __ldg(dirs + 2 * n_dirs + i)};
-            const double f = fval(m, d, Sa, Sb);
+            const float m[3] = {__ldg(dirs32 + i), __ldg(dirs32 + n_dirs + i), __ldg(dirs32 + 2 * n_dirs + i)};
+            const float f = fval32(m, d32, A32, B32);
             if (!(f > topf[K - 1]) && topi[K - 1] >= 0) {
                 // cannot enter; it may still only replace a nearby leader, which
                 // needs f > that leader's value >= the worst: nothing to do
@@ -341,9 +364,9 @@ __device__ int snsd_stage2(const double *d, const Sym &Sa, const Sym &Sb, int n_
             for (int k = 0; k < K; ++k) {
                 if (near < 0 && topi[k] >= 0) {
                     const int j = topi[k];
-                    const double c = m[0] * __ldg(dirs + j) + m[1] * __ldg(dirs + n_dirs + j) +
-                                     m[2] * __ldg(dirs + 2 * n_dirs + j);
-                    if (c > SNSD_SEP_COS) near = k;
+                    const float c = m[0] * __ldg(dirs32 + j) + m[1] * __ldg(dirs32 + n_dirs + j) +
+                                    m[2] * __ldg(dirs32 + 2 * n_dirs + j);
+                    if (c > (float)SNSD_SEP_COS) near = k;
                 }
             }
             int p;
@@ -636,7 +659,7 @@ __global__ void __launch_bounds__(128, SNSD_MINB) k_snsd_stage2(const int *__res
                                                      const int *__restrict__ pi, const int *__restrict__ pj,
                                                      const double *__restrict__ pos, const double *__restrict__ Sig,
                                                      Box3 box, int n_dirs, const double *__restrict__ dirs,
-                                                     double *__restrict__ phi,
+                                                     const float *__restrict__ dirs32, double *__restrict__ phi,
                                                      double *__restrict__ nrm, double *__restrict__ ra,
                                                      double *__restrict__ rb, int *__restrict__ status,
                                                      int64_t planes) {
@@ -648,7 +671,7 @@ __global__ void __launch_bounds__(128, SNSD_MINB) k_snsd_stage2(const int *__res
         pair_geom(k, pi, pj, pos, Sig, box, d, Sa, Sb);
         double nb[3] = {nrm[k], nrm[planes + k], nrm[2 * planes + k]};
         double f, n[3], r1[3], r2[3];
-        const int st = snsd_stage2(d, Sa, Sb, n_dirs, dirs, nb, status[k], f, n, r1, r2);
+        const int st = snsd_stage2(d, Sa, Sb, n_dirs, dirs, dirs32, nb, status[k], f, n, r1, r2);
         store_pair(k, planes, f, n, r1, r2, phi, nrm, ra, rb);
         status[k] = st;
     }
@@ -666,7 +689,8 @@ int geo_snsd(relcp_ctx *ctx, int64_t np, const int *pi, const int *pj, const dou
     CK(ctx->nlist.grow(np));
     if (ctx->dirs_n != nd) {
         CK(ctx->dirs.grow(3 * nd));
-        k_dirs<<<(nd + 127) / 128, 128, 0, ctx->stream>>>(nd, ctx->dirs.p);
+        CK(ctx->dirs32.grow(3 * nd));
+        k_dirs<<<(nd + 127) / 128, 128, 0, ctx->stream>>>(nd, ctx->dirs.p, ctx->dirs32.p);
         CKL();
         ctx->dirs_n = nd;
     }
@@ -687,8 +711,7 @@ int geo_snsd(relcp_ctx *ctx, int64_t np, const int *pi, const int *pj, const dou
                                                     ra, rb, status, planes, ctx->multi.p, ctx->counter.p + 1);
     CKL();
     k_snsd_stage2<<<148 * 8, 128, 0, ctx->stream>>>(ctx->multi.p, ctx->counter.p + 1, pi, pj, pos, Sig, bx, nd,
-                                                    ctx->dirs.p, phi,
-                                                    nrm, ra, rb, status, planes);
+                                                    ctx->dirs.p, ctx->dirs32.p, phi, nrm, ra, rb, status, planes);
     CKL();
     return RELCP_OK;
 }
