@@ -181,6 +181,29 @@ def test_fullsize_cfg4_lcp(R):
     assert 0.4 < float((lam > 0).double().mean()) < 0.9
 
 
+def test_fullsize_cfg4_6M_lcp(orc, R):
+    """cfg4-6M (c = 3 rows per link, 5.994M rows, the
+    BASELINE "~6M"): N_C > 6 N_free, so lambda is not unique (Lemma 5,
+    P:L333-373, R13); solved to r <= 1e-8 with lambda >= 0, and the returned g
+    equals the oracle's own s D^T W D lambda + q on every row (1e-12 of the
+    scale of A lambda)."""
+    sc = scenes.cfg4(c_fixed=3)
+    net = sc["network"]
+    assert len(net["ia"]) == 5_994_000
+    ctx = _ctx(R, sc, lcp_tol=1e-8, lcp_max_iter=50000)
+    bodies = R.BodyState.from_scene(sc)
+    cs = R.ConstraintStore(len(net["ia"]) + 16)
+    ctx.load_constraints(bodies, cs, net["ia"], net["ib"], net["n"], net["ra"], net["rb"], net["phi"])
+    rep = ctx.solve_lcp(bodies, cs)
+    assert rep["converged"] and rep["residual"] <= 1e-8
+    c = cs.to_numpy()
+    assert np.all(c["lam"] >= 0)
+    W = orc.body_W(sc)
+    Alam = orc.delassus_apply(W, c["ia"], c["ib"], c["n"], c["ta"], c["tb"], sc["dt"] ** 2, c["lam"])
+    assert np.max(np.abs(c["g"] - (Alam + c["q"]))) <= 1e-12 * np.max(np.abs(Alam))
+    assert np.max(np.abs(np.minimum(c["lam"], c["g"]))) <= 1e-8
+
+
 def test_fullsize_cfg3_step_planar(R):
     sc = scenes.cfg3()
     ctx = _ctx(R, sc, lcp_tol=1e-8, lcp_max_iter=3000, max_recursions=3)

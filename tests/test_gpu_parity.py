@@ -320,7 +320,10 @@ def test_generate_contacts_parity_cfg1(orc, R, cfg1_a0):
     assert n0 == len(c["ia"])
     assert np.array_equal(g["ia"], c["ia"]) and np.array_equal(g["ib"], c["ib"])
     assert np.all(g["gen"] == 0)
-    assert np.max(np.abs(g["phi"] - c["phi"])) <= 1e-12 * 10
+    # Phi within 1e-12 max(1, |d|) per pair, n within 1e-10
+    d = sc["pos"][g["ib"]] - sc["pos"][g["ia"]]
+    d -= sc["box"] * np.rint(d / sc["box"])
+    assert np.all(np.abs(g["phi"] - c["phi"]) <= 1e-12 * np.maximum(1.0, np.linalg.norm(d, axis=1)))
     assert np.max(np.abs(g["n"] - c["n"])) <= 1e-10
     assert np.max(np.abs(g["ta"] - c["ta"])) <= 1e-9 and np.max(np.abs(g["tb"] - c["tb"])) <= 1e-9
     assert np.max(np.abs(g["q"] - r["q_hist"][0])) <= 1e-11
@@ -355,6 +358,11 @@ def _compare_step(orc, R, sc, tol_cfg=1e-9, max_recursions=50, solver=0, reorder
     og, oo = _sorted_rows(g["ia"], g["ib"], g["gen"]), _sorted_rows(c["ia"], c["ib"], c["gen"])
     assert np.array_equal(g["ia"][og], c["ia"][oo]) and np.array_equal(g["ib"][og], c["ib"][oo])
     assert np.array_equal(g["gen"][og], c["gen"][oo])
+    # rows found at C^k (gen 0) have identical inputs: n within 1e-10 (SURVEY
+    # §8(c)); appended rows are evaluated at trial configurations that agree
+    # only to the configuration tolerance (R19, ~1e-9), so n to 1e-8 there
+    g0 = g["gen"][og] == 0
+    assert np.max(np.abs(g["n"][og][g0] - c["n"][oo][g0]), initial=0.0) <= 1e-10
     assert np.max(np.abs(g["n"][og] - c["n"][oo])) <= 1e-8
     pos = bodies.pos.cpu().numpy()
     dpos = pos - r["pos"]

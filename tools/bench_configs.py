@@ -56,6 +56,8 @@ def run(name):
         sc = scenes.cfg3()
     elif name == "cfg4":
         sc = scenes.cfg4()
+    elif name == "cfg4-6M":
+        sc = scenes.cfg4(c_fixed=3)
     else:
         sc = scenes.cfg5()
     gen_s = time.time() - t0
@@ -65,7 +67,7 @@ def run(name):
     bodies = R.BodyState.from_scene(sc)
     init = {k: getattr(bodies, k).clone() for k in ("pos", "quat", "vel")}
     out = dict(config=name, n_bodies=n, gen_s=gen_s)
-    if name == "cfg4":
+    if name.startswith("cfg4"):
         net = sc["network"]
         cs = R.ConstraintStore(len(net["ia"]) + 16)
         ctx.load_constraints(bodies, cs, net["ia"], net["ib"], net["n"], net["ra"], net["rb"], net["phi"])
