@@ -157,11 +157,11 @@ def with_state(sc: dict, pos, quat, vel_seed: int, name: str) -> dict:
 
 def colony_rods(seed: int = 7, n: int = 131_072, dt: float = 1e-2, patch: int = 6) -> dict:
     """The paper's colony shape class: spherocylinders
-    of diameter b = 0.5 and centreline length l ~ U(2, 4) (between l_0 and the
-    division length 2 l_0), planar, packed with the cfg3 row-patch
+    of diameter b = 0.5 and (tip-to-tip) length l ~ U(2, 4) (between l_0 and
+    the division length 2 l_0), planar, packed with the cfg3 row-patch
     construction, every cell grown by l <- l e^dt (l_dot = l) at the start of
-    the step; 2^17 cells by default.  Overdamped local drag with L = l + b
-    (R22).  Division is out of scope."""
+    the step; 2^17 cells by default.  Overdamped local drag with L = l (R22).
+    Division: drivers.colony / divide_rods (R28)."""
     return cfg3(seed=seed, n=n, patch=patch, rods=True, dt=dt)
 
 
@@ -183,7 +183,7 @@ def cfg3(seed: int = 3, n: int = 200_000, patch: int = 6, gap: float = 0.005, mi
     directors, row offsets, growth set."""
     rng = np.random.Generator(np.random.PCG64(seed))
     # tip half-length law: ellipsoid a ~ U(0.5, 1); rod (l + b)/2 with l ~ U(2, 4)
-    a_lo, a_hi = (0.5, 1.0) if not rods else (1.0 + minor, 2.0 + minor)
+    a_lo, a_hi = (0.5, 1.0) if not rods else (1.0, 2.0)  # rods: half the tip-to-tip length l ~ U(2, 4)
     # disk radius from the realised packing (~0.55 area fraction)
     area_body = math.pi * 0.5 * (a_lo + a_hi) * minor
     fill, rim = (0.55, 4.0) if not rods else (0.40, 3.0 * a_hi)  # long rods lose more at patch borders
@@ -256,8 +256,9 @@ def cfg3(seed: int = 3, n: int = 200_000, patch: int = 6, gap: float = 0.005, mi
     quat[:, 0] = np.cos(angs / 2)
     quat[:, 3] = np.sin(angs / 2)
     if rods:
-        # spherocylinder: axes = (l/2, r, r); every cell grows l <- l e^dt
-        ell = 2.0 * (majors - minor) * math.exp(dt)
+        # spherocylinder: tip-to-tip length l = 2 a, grown l <- l e^dt (R22);
+        # axes = (centreline / 2, r, r) with centreline = l - 2 r
+        ell = 2.0 * majors * math.exp(dt) - 2.0 * minor
         axes = np.stack([0.5 * ell, np.full(n, minor), np.full(n, minor)], axis=1)
         shape = np.ones(n, dtype=np.int32)
         grow[:] = True

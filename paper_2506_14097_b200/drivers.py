@@ -9,6 +9,8 @@ Scenario mechanics only (box rescale, axial growth); every time step is one
 * growth(...)      cfg3: a fixed half of the bodies grows its major semi-axis
   by `rate` at the start of every step after the first (the scene already
   holds the first step's growth; BASELINE cfg3).
+* colony(...)      the paper's colony: rods grow
+  l <- l e^dt (R22) and divide at 2 l_0 (R28, divide_rods).
 * snsd_vs_relcp(...) the paper's LCP-SNSD baseline (max_recursions = 0: the
   A_0 solution is accepted as is) against ReLCP on the same state:
   the overlap that remains at the accepted configuration.
@@ -17,6 +19,7 @@ from __future__ import annotations
 
 import math
 
+import numpy as np
 import torch
 
 from . import relcp as R
@@ -66,11 +69,113 @@ def growth(sc, steps: int = 10, rate: float = 0.01, capacity_per_body: int = 16,
     for k in range(steps):
         if k > 0:
             if rods:
-                bodies.axes[grow, 0] *= math.exp(sc["dt"])
+                grow_rods(bodies, sc["dt"], grow)
             else:
                 bodies.axes[grow, 0] += rate
         rep = ctx.step(bodies, cs)
         rep.update(step=k)
+        reps.append(rep)
+        if callback:
+            callback(k, bodies, cs, rep)
+    return reps, bodies, cs
+
+
+DIV_ANGLE = 0.01 * math.pi / 180.0  # +-0.01 degrees
+
+
+def grow_rods(bodies, dt: float, mask=None):
+    """l_dot = l on the tip-to-tip length l = 2 (axes[:, 0] + r) (P:L1030,
+    R22): l <- l e^dt, i.e. the centreline half-length a0 <- (a0 + r) e^dt - r."""
+    a = bodies.axes
+    if mask is None:
+        a[:, 0] = (a[:, 0] + a[:, 1]) * math.exp(dt) - a[:, 1]
+    else:
+        a[mask, 0] = (a[mask, 0] + a[mask, 1]) * math.exp(dt) - a[mask, 1]
+
+
+def _qmul(a, b):
+    """Hamilton product of (..., 4) quaternions (s, x, y, z)."""
+    s1, x1, y1, z1 = a.unbind(-1)
+    s2, x2, y2, z2 = b.unbind(-1)
+    return torch.stack([s1 * s2 - x1 * x2 - y1 * y2 - z1 * z2, s1 * x2 + x1 * s2 + y1 * z2 - z1 * y2,
+                        s1 * y2 - x1 * z2 + y1 * s2 + z1 * x2, s1 * z2 + x1 * y2 - y1 * x2 + z1 * s2], -1)
+
+
+def divide_rods(bodies, l0: float, rng):
+    """Cell division of the colony (reading R28).
+    Every rod whose tip-to-tip length l = 2 (axes[:, 0] + r) has reached 2 l0
+    is split at its mid cross-section into two daughters of length l / 2 (= l0
+    at l = 2 l0, so the population doubles every ln 2 under l_dot = l): centres
+    x -+ (l/4) u along the mother's axis u, centreline l/2 - 2 r, touching tip
+    to tip at x and filling the mother's extent (no new overlap).  Each daughter is
+    turned by a random +-0.01 degrees about the plane normal z (world frame,
+    q <- q_z(delta) q); the signs are drawn from `rng` (numpy Generator),
+    two per division in ascending mother order.  Daughter A keeps the
+    mother's index, daughter B is appended (mother order).  Scenario
+    mechanics between steps, on the device arrays; returns the new BodyState
+    and the number of divisions."""
+    a = bodies.axes
+    idx = torch.nonzero(2.0 * (a[:, 0] + a[:, 1]) >= 2.0 * l0).flatten()
+    m = int(idx.numel())
+    if m == 0:
+        return bodies, 0
+    q = bodies.quat[idx]
+    q = q / q.norm(dim=1, keepdim=True)
+    s, x, y, z = q.unbind(-1)
+    u = torch.stack([1 - 2 * (y * y + z * z), 2 * (x * y + s * z), 2 * (x * z - s * y)], -1)  # R(q) e_x
+    r = a[idx, 1]
+    ell = 2.0 * (a[idx, 0] + r)  # tip-to-tip length
+    off = (0.25 * ell)[:, None] * u
+    sg = torch.as_tensor(rng.choice(np.array([-1.0, 1.0]), size=(m, 2)), dtype=torch.float64, device=a.device)
+    half = 0.5 * DIV_ANGLE * sg
+    qz = torch.stack([torch.cos(half), torch.zeros_like(half), torch.zeros_like(half), torch.sin(half)], -1)
+    qa, qb = _qmul(qz[:, 0], q), _qmul(qz[:, 1], q)
+    pos = bodies.pos.clone()
+    quat = bodies.quat.clone()
+    axes = bodies.axes.clone()
+    x0 = pos[idx]
+    pos[idx] = x0 - off
+    quat[idx] = qa
+    axes[idx, 0] = 0.25 * ell - r
+    new_axes = torch.stack([0.25 * ell - r, r, a[idx, 2]], -1)
+
+    def cat(t, extra):
+        return None if t is None else torch.cat([t, extra]).contiguous()
+
+    nb = R.BodyState.__new__(R.BodyState)
+    nb.pos = cat(pos, x0 + off)
+    nb.quat = cat(quat, qb)
+    nb.axes = cat(axes, new_axes)
+    nb.vel = cat(bodies.vel, torch.zeros(m, 6, dtype=torch.float64, device=a.device))
+    nb.inv_mass = cat(bodies.inv_mass, bodies.inv_mass[idx] if bodies.inv_mass is not None else None)
+    nb.inv_inertia = cat(bodies.inv_inertia, bodies.inv_inertia[idx] if bodies.inv_inertia is not None else None)
+    nb.kinematic = cat(bodies.kinematic, bodies.kinematic[idx] if bodies.kinematic is not None else None)
+    nb.shape = cat(bodies.shape, bodies.shape[idx] if bodies.shape is not None else None)
+    nb.n = nb.pos.shape[0]
+    return nb, m
+
+
+def colony(sc, steps: int = 10, l0: float = 2.0, seed: int = 1030, capacity_per_body: int = 16, callback=None,
+           **kw):
+    """The growing and dividing colony: at the start
+    of every step after the first, every rod grows l <- l e^dt (grow_rods, R22) and the
+    rods at 2 l0 divide (divide_rods, R28); then one relcp_step.  Returns the
+    per-step reports (with the body count and divisions), the bodies, the
+    store."""
+    ctx = _ctx_for(sc, **kw)
+    bodies = R.BodyState.from_scene(sc)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    reps = []
+    cs = None
+    for k in range(steps):
+        ndiv = 0
+        if k > 0:
+            grow_rods(bodies, sc["dt"])
+            bodies, ndiv = divide_rods(bodies, l0, rng)
+        if cs is None or cs.capacity < capacity_per_body * bodies.n:
+            cs = R.ConstraintStore(2 * capacity_per_body * bodies.n + 1024)
+        rep = ctx.step(bodies, cs)
+        rep.update(step=k, n_bodies=bodies.n, divisions=ndiv)
         reps.append(rep)
         if callback:
             callback(k, bodies, cs, rep)
@@ -127,4 +232,4 @@ def box_length(phi0: float, L0: float, phi: float) -> float:
     return L0 * (phi0 / phi) ** (1.0 / 3.0)
 
 
-__all__ = ["compaction", "growth", "snsd_vs_relcp", "box_length", "math"]
+__all__ = ["compaction", "growth", "colony", "divide_rods", "grow_rods", "snsd_vs_relcp", "box_length", "math"]

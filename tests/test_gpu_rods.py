@@ -93,8 +93,8 @@ def test_rod_growth_driver(orc, R):
     ref["pos"], ref["quat"], ref["axes"] = sc["pos"].copy(), sc["quat"].copy(), sc["axes"].copy()
     n_c = []
     for k in range(3):
-        if k > 0:
-            ref["axes"][:, 0] *= math.exp(sc["dt"])
+        if k > 0:  # l_dot = l on the tip-to-tip length l = 2 (a0 + r) (R22)
+            ref["axes"][:, 0] = (ref["axes"][:, 0] + ref["axes"][:, 1]) * math.exp(sc["dt"]) - ref["axes"][:, 1]
         rr = orc.relcp_step(ref, lcp_tol=1e-12, max_recursions=3)
         ref["pos"], ref["quat"] = rr["pos"], rr["quat"]
         n_c.append(rr["n_c"])
@@ -114,3 +114,80 @@ def test_mixed_shapes_refused(R):
     with pytest.raises(R.RelcpError) as e:
         ctx.generate_contacts(bodies, cs)
     assert e.value.code == R.E_DEGENERATE
+
+
+def _divide_np(sc, l0, rng):
+    """Test-side twin of drivers.divide_rods (reading R28, P:L1030-1032,
+    P:L1056), written independently in numpy: rods of tip-to-tip length
+    l = 2 (a0 + r) >= 2 l0 become two daughters of length l/2 (centreline
+    l/2 - 2r) at x -+ (l/4) u, each turned by a random +-0.01 degrees about z;
+    daughter B appended in mother order."""
+    a = sc["axes"]
+    idx = np.flatnonzero(2.0 * (a[:, 0] + a[:, 1]) >= 2.0 * l0)
+    m = len(idx)
+    if m == 0:
+        return sc, 0
+    out = dict(sc)
+    q = sc["quat"][idx] / np.linalg.norm(sc["quat"][idx], axis=1)[:, None]
+    s, x, y, z = q.T
+    u = np.stack([1 - 2 * (y * y + z * z), 2 * (x * y + s * z), 2 * (x * z - s * y)], 1)
+    r = a[idx, 1]
+    ell = 2.0 * (a[idx, 0] + r)
+    off = (0.25 * ell)[:, None] * u
+    sg = rng.choice(np.array([-1.0, 1.0]), size=(m, 2))
+    th = 0.5 * (0.01 * math.pi / 180.0) * sg
+
+    def rot(t):  # q_z(2 t) q: (cos t, 0, 0, sin t) (x) q
+        c, sn = np.cos(t), np.sin(t)
+        return np.stack([c * s - sn * z, c * x - sn * y, c * y + sn * x, c * z + sn * s], 1)
+
+    pos, quat, axes = sc["pos"].copy(), sc["quat"].copy(), sc["axes"].copy()
+    x0 = pos[idx].copy()
+    pos[idx] = x0 - off
+    quat[idx] = rot(th[:, 0])
+    axes[idx, 0] = 0.25 * ell - r
+    new_axes = np.stack([0.25 * ell - r, r, a[idx, 2]], 1)
+    out["pos"] = np.concatenate([pos, x0 + off])
+    out["quat"] = np.concatenate([quat, rot(th[:, 1])])
+    out["axes"] = np.concatenate([axes, new_axes])
+    for k in ("vel",):
+        out[k] = np.concatenate([sc[k], np.zeros((m, 6))])
+    for k in ("inv_mass", "inv_inertia", "kinematic", "shape", "growing"):
+        if k in sc and sc[k] is not None:
+            out[k] = np.concatenate([sc[k], sc[k][idx]])
+    out["n"] = len(out["pos"])
+    return out, m
+
+
+def test_rod_division_driver(orc, R):
+    """The dividing colony (cells divide into two upon reaching
+    2 l_0, daughters turned by +-0.01 degrees): three steps of the GPU
+    driver (drivers.colony) against the oracle stepping a numpy twin of the
+    same growth and division rule (R22, R28): body counts, rows per LCP and the
+    accepted configurations agree, and every step ends below eps_NCP."""
+    from paper_2506_14097_b200 import drivers as D
+    sc = scenes.colony_rods(n=400)
+    l0, seed = 2.0, 1030
+    rng = np.random.Generator(np.random.PCG64(seed))
+    ref = dict(sc)
+    counts, n_c, divs = [], [], []
+    for k in range(3):
+        m = 0
+        if k > 0:
+            ref["axes"] = ref["axes"].copy()
+            ref["axes"][:, 0] = (ref["axes"][:, 0] + ref["axes"][:, 1]) * math.exp(sc["dt"]) - ref["axes"][:, 1]
+            ref, m = _divide_np(ref, l0, rng)
+        rr = orc.relcp_step(ref, lcp_tol=1e-12, max_recursions=5)
+        ref["pos"], ref["quat"] = rr["pos"], rr["quat"]
+        counts.append(ref["n"])
+        n_c.append(rr["n_c"])
+        divs.append(m)
+    reps, bodies, cs = D.colony(sc, steps=3, l0=l0, seed=seed, lcp_tol=1e-12, lcp_max_iter=2_000_000,
+                                max_recursions=5)
+    assert divs[1] > 0, "the recipe must divide some cells in the first steps"
+    assert [x["divisions"] for x in reps] == divs
+    assert [x["n_bodies"] for x in reps] == counts
+    assert [x["n_c"] for x in reps] == n_c
+    assert np.max(np.abs(bodies.axes.cpu().numpy() - ref["axes"])) <= 1e-15
+    assert np.max(np.abs(bodies.pos.cpu().numpy() - ref["pos"])) <= 1e-8
+    assert all(x["max_overlap"] <= sc["eps_ncp"] for x in reps)

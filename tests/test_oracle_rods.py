@@ -110,7 +110,7 @@ def test_mixed_shapes_undefined(orc):
 def test_rod_colony_recipe(orc):
     sc = scenes.colony_rods(n=1500)
     assert np.all(sc["shape"] == 1)
-    ell = 2 * sc["axes"][:, 0]
+    ell = 2 * (sc["axes"][:, 0] + sc["axes"][:, 1])  # tip-to-tip length (R22)
     assert ell.min() >= 2.0 and ell.max() <= 4.0 * math.exp(sc["dt"]) + 1e-12
     rad = orc.bounding_radius(sc["axes"], sc["shape"])
     pi, pj = orc.broadphase(sc["pos"], rad, None, 0.1)
