@@ -87,6 +87,10 @@ typedef struct relcp_params {
                              when fewer than RELCP_REORDER_COHERENT of the
                              consecutive caller bodies (b, b+1) lie in the same
                              or adjacent cells], _ON (see relcp_step)              */
+    int32_t layout;       /* operator layout of the LCP solve: RELCP_LAYOUT_CSR
+                             [default] | RELCP_LAYOUT_JDS (used when the store is
+                             sorted by ia and every row has t . n ~ 0; else
+                             CSR).  Results agree to rounding. */
 } relcp_params;
 
 #define RELCP_REORDER_OFF 0
@@ -94,6 +98,19 @@ typedef struct relcp_params {
 #define RELCP_REORDER_ON 2
 #define RELCP_REORDER_MIN_BODIES 65536
 #define RELCP_REORDER_COHERENT 0.5
+
+/* Operator layout (params.layout; DESIGN.md §5 "K6 layouts").  CSR: K6 reads
+ * the a-side rows in the store's order through shared-memory tiles and the
+ * b-side entries from a CSR copy.  JDS: op_prepare permutes the rows of every
+ * 32-body group into a per-warp jagged-diagonal order (lanes sorted by
+ * degree, column j = every lane's j-th row); the solve runs on a private copy
+ * in that order (ids, compact rows, q, lambda, g) and writes lambda and g
+ * back in the caller's row order; K6 streams whole columns and sums them
+ * from shared memory without bank conflicts.  Measured equal in time to CSR
+ * at cfg5 with ~20 % less DRAM traffic (profiles/README.md), hence not the
+ * default.  The fused APGD solver always uses CSR.                         */
+#define RELCP_LAYOUT_CSR 0
+#define RELCP_LAYOUT_JDS 1
 
 /* LCP solvers (the paper names only the family; reading R1):
  *   BB   Barzilai-Borwein projected gradient (alternating BB1 / BB2 steps);
@@ -317,7 +334,11 @@ int relcp_get_pairs(relcp_ctx *ctx, int32_t *pi, int32_t *pj, int64_t cap, int64
  *   n_guard                 SNSD-scanned pairs inside the R14 guard band
  *                           |Phi - threshold| < 1e-10 (generation: cutoff;
  *                           checks: -eps_ncp), over every generate / check
- *                           since the reset (timing off or on). */
+ *                           since the reset (timing off or on);
+ *   jds_solves              LCP solves run on the JDS operator layout since
+ *                           the reset (params.layout);
+ *   op_layout               layout of the operator prepared last
+ *                           (RELCP_LAYOUT_CSR or RELCP_LAYOUT_JDS). */
 typedef struct relcp_stats {
     int64_t launches;
     int64_t lcp_iterations;
@@ -327,6 +348,9 @@ typedef struct relcp_stats {
     int64_t split_timed;
     double iter_ms;
     int64_t n_guard;
+    int64_t jds_solves;
+    int32_t op_layout;
+    int32_t pad;
 } relcp_stats;
 int relcp_get_stats(relcp_ctx *ctx, relcp_stats *out);
 int relcp_reset_stats(relcp_ctx *ctx);

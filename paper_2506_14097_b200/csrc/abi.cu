@@ -33,6 +33,7 @@ static int check_params(const relcp_params *p) {
     if (p->solver != RELCP_SOLVER_BB && p->solver != RELCP_SOLVER_APGD && p->solver != RELCP_SOLVER_APGD_FUSED)
         return 0;
     if (p->reorder < RELCP_REORDER_OFF || p->reorder > RELCP_REORDER_ON) return 0;
+    if (p->layout != RELCP_LAYOUT_CSR && p->layout != RELCP_LAYOUT_JDS) return 0;
     return 1;
 }
 
@@ -406,6 +407,7 @@ void relcp_default_params(relcp_params *p) {
     p->xi = 1.0;
     p->n_dirs = 256;
     p->reorder = RELCP_REORDER_AUTO;
+    p->layout = RELCP_LAYOUT_CSR;
 }
 
 int relcp_create(relcp_ctx **out, const relcp_params *p, void *cuda_stream) {
@@ -708,6 +710,9 @@ int relcp_get_stats(relcp_ctx *ctx, relcp_stats *out) {
     out->split_timed = ctx->split_timed;
     out->iter_ms = ctx->iter_ms;
     out->n_guard = ctx->n_guard_total;
+    out->jds_solves = ctx->jds_solves;
+    out->op_layout = ctx->op_jds ? RELCP_LAYOUT_JDS : RELCP_LAYOUT_CSR;
+    out->pad = 0;
     return RELCP_OK;
 }
 
@@ -718,6 +723,7 @@ int relcp_reset_stats(relcp_ctx *ctx) {
     ctx->iter_timed = ctx->split_timed = 0;
     ctx->scatter_ms = ctx->gather_ms = ctx->iter_ms = 0.0;
     ctx->n_guard_total = 0;
+    ctx->jds_solves = 0;
     return RELCP_OK;
 }
 

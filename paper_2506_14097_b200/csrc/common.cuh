@@ -53,6 +53,14 @@ struct DevBuf {
         p = nullptr;
         cap = 0;
     }
+    void swap(DevBuf &o) {
+        T *tp = p;
+        p = o.p;
+        o.p = tp;
+        const size_t tc = cap;
+        cap = o.cap;
+        o.cap = tc;
+    }
     DevBuf() = default;
     DevBuf(const DevBuf &) = delete;
     DevBuf &operator=(const DevBuf &) = delete;
@@ -136,6 +144,20 @@ struct relcp_ctx {
     DevBuf<double> vtmp;     // (nc) power iteration / apply scratch
     DevBuf<double> apgd_buf; // (2, nc) APGD second iterate (x', g'); fused BB: x'
     DevBuf<double> Fa;       // (6, nb) fused BB: a-side wrench sums of the next iterate
+    // JDS operator layout (params.layout, operator.cu "JDS"): rows in slot order
+    int op_jds = 0;          // the operator was prepared in the JDS layout
+    int jds_enable = 1;      // 0: never (domain-decomposition part contexts)
+    int64_t jds_solves = 0;  // solves on the JDS layout since the stats reset
+    DevBuf<int> jperm;       // (nc) slot -> store row
+    DevBuf<int> jiperm;      // (nc) store row -> slot
+    DevBuf<int> jameta;      // (32 nwarp) a-side lane -> degree << 5 | local body
+    DevBuf<int> jbmeta;      // (32 nwarp) b-side lane -> degree << 5 | local body
+    DevBuf<int> jbcid;       // (nc) b-side entry (JDS order) -> slot of its row
+    DevBuf<double> jbpay;    // (4, nc) b-side entry compact payload (u, v, t_b,j1, t_b,j2)
+    DevBuf<int> jia, jib;    // (nc) ids in slot order
+    DevBuf<double> jq, jx, jg;  // (nc) q, lambda, g in slot order (the solve's private view)
+    DevBuf<double> jtmp;     // (nc) slot-order copy of a caller's x (apply / wrench / check)
+    DevBuf<double> rc2;      // (6, nc) permutation scratch for rc
     LcpState *st_host = nullptr;  // pinned mirror
 
     // step state (from generate_contacts at C^k)
@@ -225,9 +247,13 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
 int op_build_W(relcp_ctx *ctx, const relcp_bodies *b, double *W);
 // scatter followed by W: U = W D x_eff; mode 0 x_eff = x, 1 BB projected step,
 // 2 APGD projected step from (x, g) / (xb, gb) (device parity picks current)
+// slots: x / g / xb / gb are in the JDS slot order (the solve's private view);
+// otherwise (store order) a JDS operator first permutes x into slot order
 int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int mode,
                const double *xscale_dev, double *U, double *F, const double *xb = nullptr,
-               const double *gb = nullptr);
+               const double *gb = nullptr, int slots = 0);
+// JDS operator: cs is either the solve's slot-order view (cs->ia == ctx->jia.p)
+// or the caller's store (y is then written through the slot -> row permutation)
 int op_gather_apply(relcp_ctx *ctx, const relcp_constraints *cs, const double *U, double *y, double scale,
                     int norm2, double *acc_out = nullptr);
 // fused BB row pass (g_{k+1}, x_{k+2}, a-side sums Fa, BB reductions)

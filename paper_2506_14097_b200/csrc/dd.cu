@@ -425,6 +425,7 @@ extern "C" int relcp_dd_create(relcp_dd **out, const relcp_params *p, void *stre
         delete dd;
         return rc;
     }
+    dd->ctx->jds_enable = 0;  // parts run the CSR layout (halo partials in body order)
     dd->K = nparts;
     dd->rank = rank;
     dd->off.assign(part_off, part_off + nparts + 1);
@@ -488,6 +489,7 @@ extern "C" int relcp_dd_load(relcp_dd *dd, const relcp_bodies *b, const relcp_co
         P->n_loc = n_own + ng;
         int rc = relcp_create(&P->ctx, &ctx->p, ctx->stream);
         if (rc != RELCP_OK) return set_err(ctx, rc, "dd_load: part context");
+        P->ctx->jds_enable = 0;
         P->empty = P->n_loc == 0;  // keeps its LCP state (reductions), no operator
         if (P->empty) continue;
         const int64_t nl = P->n_loc;

@@ -367,11 +367,62 @@ static double op_scale(const relcp_ctx *ctx) {
     return ctx->p.dynamics == RELCP_INERTIAL ? dt * dt : dt;  // P:L553 vs P:L512
 }
 
+// JDS layout: the solve's private slot-order view in / out
+__global__ void k_jds_in(int64_t nc, const int *__restrict__ perm, const double *__restrict__ lam,
+                         const double *__restrict__ q, double *__restrict__ x, double *__restrict__ qs) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
+        const int r = perm[a];
+        x[a] = lam[r];
+        qs[a] = q[r];
+    }
+}
+__global__ void k_jds_out(int64_t nc, const int *__restrict__ perm, const double *__restrict__ x,
+                          const double *__restrict__ g, double *__restrict__ lam, double *__restrict__ gout) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
+        const int r = perm[a];
+        lam[r] = x[a];
+        gout[r] = g[a];
+    }
+}
+
+static int lcp_solve_view(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relcp_solve_report *rep);
+
 int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relcp_solve_report *rep) {
     const int64_t nc = cs->count, nb = b->n;
     if (!cs->q || !cs->lambda || !cs->g) return set_err(ctx, RELCP_E_ARG, "solve: q, lambda and g are required");
     if (ctx->op_nc != nc || ctx->op_nb != nb || ctx->op_key_ia != cs->ia) CKS(op_prepare(ctx, b, cs));
+    if (ctx->op_jds && ctx->p.solver == RELCP_SOLVER_APGD_FUSED) {  // the fused row pass needs the CSR layout
+        ctx->op_nc = -1;
+        CKS(op_prepare(ctx, b, cs));
+    }
     PHASE(ctx, "solve.prepare");
+    if (!ctx->op_jds || nc == 0) return lcp_solve_view(ctx, b, cs, rep);
+    // JDS: solve on the slot-order view (ids, q, lambda, g; compact rows in ctx->rc), then
+    // write lambda and g back in the caller's row order
+    CK(ctx->jq.grow(nc));
+    CK(ctx->jx.grow(nc));
+    CK(ctx->jg.grow(nc));
+    k_jds_in<<<grid_for(nc), RELCP_NT, 0, ctx->stream>>>(nc, ctx->jperm.p, cs->lambda, cs->q, ctx->jx.p, ctx->jq.p);
+    CKL();
+    relcp_constraints v = *cs;
+    v.ia = ctx->jia.p;
+    v.ib = ctx->jib.p;
+    v.q = ctx->jq.p;
+    v.lambda = ctx->jx.p;
+    v.g = ctx->jg.p;
+    ++ctx->jds_solves;
+    const int rc = lcp_solve_view(ctx, b, &v, rep);
+    if (rc < 0 && rc != RELCP_E_NAN) return rc;
+    k_jds_out<<<grid_for(nc), RELCP_NT, 0, ctx->stream>>>(nc, ctx->jperm.p, ctx->jx.p, ctx->jg.p, cs->lambda, cs->g);
+    CKL();
+    CK(cudaStreamSynchronize(ctx->stream));
+    return rc;
+}
+
+// the solve proper on cs: the caller's store, or the JDS slot-order view (op_scatter slots)
+static int lcp_solve_view(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relcp_solve_report *rep) {
+    const int64_t nc = cs->count, nb = b->n;
+    const int sl = ctx->op_jds;  // x / g / q arrays of cs are in slot order
     CK(ctx->vtmp.grow(nc > 0 ? nc : 1));
     const double s = op_scale(ctx);
     cudaStream_t st = ctx->stream;
@@ -391,12 +442,12 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
     k_fill<<<gridc, RELCP_NT, 0, st>>>(nc, ctx->vtmp.p, 1.0);
     CKL();
     for (int it = 0; it < ctx->p.power_iters; ++it) {
-        CKS(op_scatter(ctx, nb, ctx->vtmp.p, nullptr, 0, &ctx->st.p->pnorm, ctx->U.p, nullptr));
+        CKS(op_scatter(ctx, nb, ctx->vtmp.p, nullptr, 0, &ctx->st.p->pnorm, ctx->U.p, nullptr, nullptr, nullptr, sl));
         CKS(op_gather_apply(ctx, cs, ctx->U.p, ctx->vtmp.p, s, 1));
     }
     PHASE(ctx, "solve.power");
     // g_0 = A x_0 + q
-    CKS(op_scatter(ctx, nb, cs->lambda, nullptr, 0, nullptr, ctx->U.p, nullptr));
+    CKS(op_scatter(ctx, nb, cs->lambda, nullptr, 0, nullptr, ctx->U.p, nullptr, nullptr, nullptr, sl));
     const bool cr = ctx->op_compact != 0;
     const int gridi = cr ? grid_for(nc, RELCP_NT, ITER_MINB_CR) : gridc;  // iteration kernels: one wave
 #define ROWS_ARGS nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->op_rs, ctx->rc.p
@@ -472,7 +523,7 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
                 continue;
             }
             if (ev_on) CK(cudaEventRecord(ctx->ev[3 * j], st));
-            CKS(op_scatter(ctx, nb, cs->lambda, cs->g, apgd ? 2 : 1, nullptr, ctx->U.p, nullptr, xB, gB));
+            CKS(op_scatter(ctx, nb, cs->lambda, cs->g, apgd ? 2 : 1, nullptr, ctx->U.p, nullptr, xB, gB, sl));
             if (ev_on) CK(cudaEventRecord(ctx->ev[3 * j + 1], st));
             if (apgd && cr)
                 k_apgd_iter<true><<<gridi, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g, xB,

@@ -180,6 +180,114 @@ __global__ void k_compact(int64_t nc, int64_t cap, const double *__restrict__ n,
     if (__any_sync(__activemask(), bad) && (threadIdx.x & 31) == 0) atomicOr(nonorth, 1);
 }
 
+// ------------------------------------------------------------ JDS layout (params.layout)
+// Per 32-body group (one warp of K6): the group's a-side rows are the store
+// range [pa[b0], pa[b0 + 32]) and its b-side entries the CSR range
+// [row_ptr[b0], row_ptr[b0 + 32]).  Each range is laid out as a jagged
+// diagonal: lanes sorted by degree (descending, ties by body), column j holds
+// the j-th entry of every lane with degree > j, so column j is lanes
+// 0 .. h_j - 1 at offset base + sum_{j' < j} h_j' (h_j = popc(ballot(deg > j)),
+// nothing stored).  meta[32 w + rank] = degree << 5 | local body.  A lane's
+// entries keep their order (its rows in store order, its b-side entries
+// sorted by constraint), so the summation order of every body is fixed.
+//   a-side: perm[slot] = store row, iperm[row] = slot;
+//   b-side: bcid[pos] = slot of the entry's row, bpay = (u, v, t_b,j1, t_b,j2)
+//           of that row from the slot-order compact planes.
+template <bool ASIDE>
+__global__ void k_jds_side(int64_t nb, const int *__restrict__ ptr, int *__restrict__ meta, int *__restrict__ perm,
+                           int *__restrict__ iperm, const int *__restrict__ ecid, const int *__restrict__ jiperm,
+                           const double *__restrict__ rcs, int64_t rs, int *__restrict__ bcid,
+                           double *__restrict__ bpay) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarp = (nb + 31) >> 5;
+    const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nwarp; w += wstride) {
+        const int64_t b0 = w << 5, b = b0 + lane;
+        const int s0 = b < nb ? ptr[b] : 0;
+        const int deg = b < nb ? ptr[b + 1] - s0 : 0;
+        int r = 0;
+        for (int m = 0; m < 32; ++m) {
+            const int dm = __shfl_sync(0xffffffffu, deg, m);
+            r += (dm > deg) || (dm == deg && m < lane);
+        }
+        meta[b0 + r] = deg << 5 | lane;
+        const int maxd = __reduce_max_sync(0xffffffffu, deg);
+        int off = ptr[b0];
+        for (int j = 0; j < maxd; ++j) {
+            const int h = __popc(__ballot_sync(0xffffffffu, deg > j));
+            if (j < deg) {
+                const int pos = off + r, src = s0 + j;
+                if (ASIDE) {
+                    perm[pos] = src;
+                    iperm[src] = pos;
+                } else {
+                    const int row = ecid[src] & (EKEY_SIDE - 1);
+                    const int slot = jiperm[row];
+                    bcid[pos] = slot;
+                    bpay[pos] = rcs[slot];
+                    bpay[rs + pos] = rcs[rs + slot];
+                    bpay[2 * rs + pos] = rcs[4 * rs + slot];
+                    bpay[3 * rs + pos] = rcs[5 * rs + slot];
+                }
+            }
+            off += h;
+        }
+    }
+}
+
+// slot-order copies of the compact rows and the ids
+__global__ void k_perm_rows(int64_t nc, const int *__restrict__ perm, const double *__restrict__ rc,
+                            double *__restrict__ rc2, const int32_t *__restrict__ ia, const int32_t *__restrict__ ib,
+                            int32_t *__restrict__ pia, int32_t *__restrict__ pib) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nc; s += (int64_t)gridDim.x * blockDim.x) {
+        const int r = perm[s];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) rc2[k * nc + s] = rc[k * nc + r];
+        pia[s] = ia[r];
+        pib[s] = ib[r];
+    }
+}
+
+// out[s] = in[perm[s]] (store order -> slot order)
+__global__ void k_perm_gather(int64_t nc, const int *__restrict__ perm, const double *__restrict__ in,
+                              double *__restrict__ out) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nc; s += (int64_t)gridDim.x * blockDim.x)
+        out[s] = in[perm[s]];
+}
+
+static int op_prepare_jds(relcp_ctx *ctx, int64_t nb, int64_t nc, const relcp_constraints *cs) {
+    const int64_t nwarp = (nb + 31) / 32;
+    CK(ctx->jperm.grow(nc));
+    CK(ctx->jiperm.grow(nc));
+    CK(ctx->jameta.grow(32 * nwarp));
+    CK(ctx->jbmeta.grow(32 * nwarp));
+    CK(ctx->jbcid.grow(nc));
+    CK(ctx->jbpay.grow(4 * nc));
+    CK(ctx->jia.grow(nc));
+    CK(ctx->jib.grow(nc));
+    CK(ctx->rc2.grow(6 * nc));
+    const unsigned gw = (unsigned)grid_for(32 * nwarp, 256, 8);
+    // a-side: slot order of the rows
+    k_jds_side<true><<<gw, 256, 0, ctx->stream>>>(nb, ctx->pa.p, ctx->jameta.p, ctx->jperm.p, ctx->jiperm.p, nullptr,
+                                                  nullptr, nullptr, 0, nullptr, nullptr);
+    CKL();
+    k_perm_rows<<<grid_for(nc), RELCP_NT, 0, ctx->stream>>>(nc, ctx->jperm.p, ctx->rc.p, ctx->rc2.p, cs->ia, cs->ib,
+                                                            ctx->jia.p, ctx->jib.p);
+    CKL();
+    ctx->rc.swap(ctx->rc2);  // rc: slot order from here on
+    // b-side: CSR of the b-side entries (sorted by constraint), then its JDS
+    CK(cudaMemsetAsync(ctx->fill.p, 0, sizeof(int) * nb, ctx->stream));
+    k_fill_slots<<<grid_for(nc), RELCP_NT, 0, ctx->stream>>>(nc, cs->ia, cs->ib, ctx->row_ptr.p, ctx->fill.p,
+                                                             ctx->ecid.p, 1);
+    CKL();
+    k_sort_segments<<<grid_for(nb, 128), 128, 0, ctx->stream>>>(nb, ctx->row_ptr.p, ctx->ecid.p);
+    CKL();
+    k_jds_side<false><<<gw, 256, 0, ctx->stream>>>(nb, ctx->row_ptr.p, ctx->jbmeta.p, nullptr, nullptr, ctx->ecid.p,
+                                                   ctx->jiperm.p, ctx->rc.p, nc, ctx->jbcid.p, ctx->jbpay.p);
+    CKL();
+    return RELCP_OK;
+}
+
 int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *cs) {
     if (!b || !cs || b->n <= 0) return set_err(ctx, RELCP_E_ARG, "prepare: empty bodies");
     const int64_t nb = b->n, nc = cs->count, E = 2 * nc;
@@ -216,8 +324,12 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
     CK(cudaStreamSynchronize(ctx->stream));
     if (flags[0]) return set_err(ctx, RELCP_E_ARG, "prepare: body index out of range or ia == ib");
     ctx->op_compact = nc > 0 && !flags[1];
+    const bool jds = ctx->jds_enable && sorted && ctx->op_compact && ctx->p.solver != RELCP_SOLVER_APGD_FUSED &&
+                     ctx->p.layout == RELCP_LAYOUT_JDS;
+    ctx->op_jds = jds;
+    if (jds) CKS(op_prepare_jds(ctx, nb, nc, cs));
     const int64_t Ee = sorted ? nc : E;  // CSR entries: b-side only when sorted
-    if (nc > 0) {
+    if (nc > 0 && !jds) {
         CK(cudaMemsetAsync(ctx->fill.p, 0, sizeof(int) * nb, ctx->stream));
         k_fill_slots<<<grid_for(nc), RELCP_NT, 0, ctx->stream>>>(nc, cs->ia, cs->ib, ctx->row_ptr.p, ctx->fill.p,
                                                                  ctx->ecid.p, sorted);
@@ -408,8 +520,217 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
     }
 }
 
+// ------------------------------------------------------------ scatter, JDS layout (K6)
+// Same operator as k_scatter (U_b = W_b sum_e w_e x_eff, MODE 0 / 1 / 2) on the
+// JDS layout (op_prepare_jds): one warp per 32-body group.  The warp's
+// entries are streamed in chunks of whole columns (<= JT_TILE entries), one
+// entry per lane and trip with every lane active (coalesced loads, x_eff and
+// the row decode done once per entry), the 6-vector contributions staged in
+// shared memory as three double2 planes in entry order; then lane r sums its
+// column entries, which sit at consecutive positions across lanes (column j:
+// lanes 0 .. h_j - 1), so the shared-memory reads are conflict-free.
+#ifndef JDS_WPB
+#define JDS_WPB 4
+#endif
+#ifndef JT_TILE
+#define JT_TILE 64
+#endif
+#ifndef JT_MINB
+#define JT_MINB 8
+#endif
+template <int MODE>
+__global__ void __launch_bounds__(32 * JDS_WPB, JT_MINB) k_scatter_jt(
+    int64_t nb, int64_t rs, const int *__restrict__ pa, const int *__restrict__ row_ptr,
+    const int *__restrict__ ameta, const int *__restrict__ bmeta, const double *__restrict__ rc,
+    const int *__restrict__ bcid, const double *__restrict__ bpay, const double *__restrict__ x,
+    const double *__restrict__ g, const double *__restrict__ xb, const double *__restrict__ gb,
+    const LcpState *__restrict__ st, const double *__restrict__ xscale, const double *__restrict__ W,
+    double *__restrict__ U, double *__restrict__ Fout) {
+    __shared__ double2 sm[JDS_WPB][3][JT_TILE];
+    __shared__ double sa_[JDS_WPB][6][32];
+    double alpha = 0.0, beta = 0.0, tl = 1.0;
+    bool fix = false;
+    const double *xc = x, *gc = g, *xp = xb, *gp = gb;
+    if (MODE != 0) {
+        if (st->done) return;
+        alpha = st->alpha;
+    }
+    if (MODE == 1) {
+        if (st->par) {
+            xc = xb; gc = gb; xp = x; gp = g;
+        }
+        fix = st->fix != 0;
+        tl = st->t_ls;
+    }
+    if (MODE == 2) {
+        beta = st->beta;
+        if (st->par) {
+            xc = xb; gc = gb; xp = x; gp = g;
+        }
+    }
+    const double sc = xscale ? *xscale : 1.0;
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    double2(*c6)[JT_TILE] = sm[wl];
+    double(*sa)[32] = sa_[wl];
+    auto xeff = [&](int c) {
+        double xv;
+        if (MODE == 0) {
+            xv = xc[c];
+        } else if (MODE == 1) {
+            double x0 = xc[c], g0 = gc[c];
+            if (fix) {
+                const double xq = xp[c], gq = gp[c];
+                x0 = fma(tl, x0 - xq, xq);
+                g0 = fma(tl, g0 - gq, gq);
+            }
+            xv = fmax(0.0, x0 - alpha * g0);
+        } else {
+            const double x0 = xc[c], g0 = gc[c];
+            const double y = x0 + beta * (x0 - xp[c]), gy = g0 + beta * (g0 - gp[c]);
+            xv = fmax(0.0, y - alpha * gy);
+        }
+        return xv * sc;
+    };
+    // one side of the warp's group: entries [base, base + sum_j h_j) in JDS
+    // order, lane degree deg; fetch(pos, v[6]) forms one entry's contribution
+    auto side = [&](int base, int deg, double (&f)[6], auto &&fetch) {
+        const int maxd = __reduce_max_sync(0xffffffffu, deg);
+        int j = 0, off = base;
+        while (j < maxd) {
+            int j1 = j, tot = 0;
+            while (j1 < maxd) {  // whole columns, <= JT_TILE entries
+                const int h = __popc(__ballot_sync(0xffffffffu, deg > j1));
+                if (tot + h > JT_TILE) break;
+                tot += h;
+                ++j1;
+            }
+#pragma unroll
+            for (int i = 0; i < JT_TILE / 32; ++i) {
+                const int p = lane + 32 * i;
+                if (p < tot) {
+                    double v[6];
+                    fetch(off + p, v);
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) c6[k][p] = make_double2(v[2 * k], v[2 * k + 1]);
+                }
+            }
+            __syncwarp();
+            int o = 0;
+            for (int jj = j; jj < j1; ++jj) {
+                const int h = __popc(__ballot_sync(0xffffffffu, deg > jj));
+                if (lane < h) {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        const double2 c = c6[k][o + lane];
+                        f[2 * k] += c.x;
+                        f[2 * k + 1] += c.y;
+                    }
+                }
+                o += h;
+            }
+            __syncwarp();
+            off += tot;
+            j = j1;
+        }
+    };
+    auto contrib = [](double u, double v, double t1, double t2, double xe, double (&o)[6]) {
+        const CNormal c = cn_decode(u, v);
+        double t[3];
+        t_expand(c, t1, t2, t);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            o[k] = c.n[k] * xe;
+            o[3 + k] = t[k] * xe;
+        }
+    };
+    const int64_t nwarp = (nb + 31) >> 5;
+    const int64_t wstep = (int64_t)gridDim.x * JDS_WPB;
+    for (int64_t w = blockIdx.x * (int64_t)JDS_WPB + wl; w < nwarp; w += wstep) {
+        const int64_t b0 = w << 5;
+        const int64_t b = b0 + lane;
+        const bool own = b < nb;
+        const int last = nb - b0 < 32 ? (int)(nb - b0 - 1) : 31;
+        const int am = ameta[b0 + lane], bm = bmeta[b0 + lane];
+        const int cA0 = pa[b0], cB0 = row_ptr[b0];
+        double f[6] = {0, 0, 0, 0, 0, 0};
+        // a-side: -[n; t_a] x_eff at consecutive slots
+        side(cA0, am >> 5, f, [&](int s, double (&v)[6]) {
+            contrib(rc[s], rc[rs + s], rc[2 * rs + s], rc[3 * rs + s], -xeff(s), v);
+        });
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            sa[k][am & 31] = f[k];
+            f[k] = 0.0;
+        }
+        // b-side: +[n; t_b] x_eff, x / g gathered at the entries' slots
+        side(cB0, bm >> 5, f, [&](int e, double (&v)[6]) {
+            const int c = bcid[e];
+            contrib(bpay[e], bpay[rs + e], bpay[2 * rs + e], bpay[3 * rs + e], xeff(c), v);
+        });
+        double *flat = &c6[0][0].x;  // 3 x JT_TILE double2 >= 2 x 192 doubles
+        static_assert(6 * JT_TILE >= 384, "JT_TILE too small for the U / F staging");
+#pragma unroll
+        for (int k = 0; k < 6; ++k) flat[k * 32 + (bm & 31)] = f[k];
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 6; ++k) f[k] = sa[k][lane] + flat[k * 32 + lane];
+        __syncwarp();
+        double u[6] = {0, 0, 0, 0, 0, 0};
+        if (own) {
+            const double w0 = W[b], s00 = W[nb + b], s01 = W[2 * nb + b], s02 = W[3 * nb + b], s11 = W[4 * nb + b],
+                         s12 = W[5 * nb + b], s22 = W[6 * nb + b];
+            u[0] = w0 * f[0];
+            u[1] = w0 * f[1];
+            u[2] = w0 * f[2];
+            u[3] = s00 * f[3] + s01 * f[4] + s02 * f[5];
+            u[4] = s01 * f[3] + s11 * f[4] + s12 * f[5];
+            u[5] = s02 * f[3] + s12 * f[4] + s22 * f[5];
+        }
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            flat[6 * lane + k] = u[k];
+            flat[192 + 6 * lane + k] = f[k];
+        }
+        __syncwarp();
+        const int64_t nvals = 6 * (int64_t)(last + 1);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            const int m = lane + 32 * i;
+            if (m < nvals) {
+                U[6 * b0 + m] = flat[m];
+                if (Fout) Fout[6 * b0 + m] = flat[192 + m];
+            }
+        }
+        __syncwarp();
+    }
+}
+
 int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int mode, const double *xscale_dev,
-               double *U, double *F, const double *xb, const double *gb) {
+               double *U, double *F, const double *xb, const double *gb, int slots) {
+    if (ctx->op_jds) {
+        const int64_t nc = ctx->op_nc;
+        if (!slots) {  // caller's store order: apply / wrench / the check's U_c
+            if (mode != 0) return set_err(ctx, RELCP_E_STATE, "JDS scatter: store-order input is apply-only");
+            CK(ctx->jtmp.grow(nc));
+            k_perm_gather<<<grid_for(nc), RELCP_NT, 0, ctx->stream>>>(nc, ctx->jperm.p, x, ctx->jtmp.p);
+            CKL();
+            x = ctx->jtmp.p;
+        }
+        const int64_t nwarp = (nb + 31) / 32;
+        const int minb = JT_MINB;
+        int64_t grid = (nwarp + JDS_WPB - 1) / JDS_WPB;
+        if (grid > (int64_t)RELCP_SM_COUNT * minb * SCATTER_WAVES) grid = (int64_t)RELCP_SM_COUNT * minb * SCATTER_WAVES;
+        if (grid < 1) grid = 1;
+#define JDS_ARGS nb, nc, ctx->pa.p, ctx->row_ptr.p, ctx->jameta.p, ctx->jbmeta.p, ctx->rc.p, ctx->jbcid.p, \
+                 ctx->jbpay.p, x, g, xb, gb, ctx->st.p, xscale_dev, ctx->W.p, U, F
+        if (mode < 0 || mode > 2) return set_err(ctx, RELCP_E_STATE, "JDS scatter: mode %d unsupported", mode);
+        if (mode == 1) k_scatter_jt<1><<<(unsigned)grid, 32 * JDS_WPB, 0, ctx->stream>>>(JDS_ARGS);
+        else if (mode == 2) k_scatter_jt<2><<<(unsigned)grid, 32 * JDS_WPB, 0, ctx->stream>>>(JDS_ARGS);
+        else k_scatter_jt<0><<<(unsigned)grid, 32 * JDS_WPB, 0, ctx->stream>>>(JDS_ARGS);
+#undef JDS_ARGS
+        CKL();
+        return RELCP_OK;
+    }
     const int64_t E = ctx->op_sorted ? ctx->op_nc : 2 * ctx->op_nc;
     const int64_t nwarp = (nb + 31) / 32;
     int64_t grid = (nwarp + SCATTER_WPB - 1) / SCATTER_WPB;
@@ -583,7 +904,8 @@ __global__ void __launch_bounds__(RELCP_NT, CR ? GATHER_MINB_CR : 4) k_gather(in
                                                      int64_t rs, const double *__restrict__ rc,
                                                      const double *__restrict__ U, double scale,
                                                      double *__restrict__ y, int norm2, double *part,
-                                                     unsigned *counter, LcpState *st, double *acc_out) {
+                                                     unsigned *counter, LcpState *st, double *acc_out,
+                                                     const int *__restrict__ yperm) {
     __shared__ double sh[32];
     double acc[1] = {0.0};
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -599,7 +921,7 @@ __global__ void __launch_bounds__(RELCP_NT, CR ? GATHER_MINB_CR : 4) k_gather(in
         for (int u = 0; u < GATHER_ILP; ++u) {
             const int64_t a = a0 + u * stride;
             if (a >= nc) continue;
-            y[a] = v[u];
+            y[yperm ? yperm[a] : a] = v[u];  // JDS operator, caller's store order: slot -> row
             acc[0] = fma(v[u], v[u], acc[0]);
         }
     }
@@ -619,14 +941,21 @@ int op_gather_apply(relcp_ctx *ctx, const relcp_constraints *cs, const double *U
     const int64_t nc = cs->count;
     if (nc == 0) return RELCP_OK;
     const int grid = grid_for(nc, RELCP_NT, ctx->op_compact ? GATHER_MINB_CR : 4);
+    const int32_t *ia = cs->ia, *ib = cs->ib;
+    const int *yperm = nullptr;
+    if (ctx->op_jds && cs->ia != ctx->jia.p) {  // caller's store: rows from the slot order, y through perm
+        ia = ctx->jia.p;
+        ib = ctx->jib.p;
+        yperm = ctx->jperm.p;
+    }
     if (ctx->op_compact)
-        k_gather<true><<<grid, RELCP_NT, 0, ctx->stream>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb,
+        k_gather<true><<<grid, RELCP_NT, 0, ctx->stream>>>(nc, cs->capacity, ia, ib, cs->n, cs->ta, cs->tb,
                                                            ctx->op_rs, ctx->rc.p, U, scale, y, norm2, ctx->partials.p,
-                                                           ctx->counter.p, ctx->st.p, acc_out);
+                                                           ctx->counter.p, ctx->st.p, acc_out, yperm);
     else
-        k_gather<false><<<grid, RELCP_NT, 0, ctx->stream>>>(nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb,
+        k_gather<false><<<grid, RELCP_NT, 0, ctx->stream>>>(nc, cs->capacity, ia, ib, cs->n, cs->ta, cs->tb,
                                                             ctx->op_rs, ctx->rc.p, U, scale, y, norm2, ctx->partials.p,
-                                                            ctx->counter.p, ctx->st.p, acc_out);
+                                                            ctx->counter.p, ctx->st.p, acc_out, yperm);
     CKL();
     return RELCP_OK;
 }

@@ -32,10 +32,11 @@ def _ctx(R, sc, **kw):
     return R.Context(**p)
 
 
-@pytest.mark.parametrize("shuffled", [False, True])
-def test_fullsize_delassus_apply(orc, R, shuffled):
+@pytest.mark.parametrize("shuffled,layout", [(False, 0), (True, 0), (False, 1)])
+def test_fullsize_delassus_apply(orc, R, shuffled, layout):
     """2M bodies, 10M rows (cfg5 scale): every output against the oracle at
-    1e-12; the shuffled store exercises the general (unsorted) CSR path."""
+    1e-12; the shuffled store exercises the general (unsorted) CSR path,
+    layout 1 the JDS operator."""
     b, ia, ib, n, ra, rb = scenes.random_constraint_network(2_000_000, 10_000_000, 77)
     if shuffled:
         p = np.random.default_rng(5).permutation(len(ia))
@@ -46,10 +47,11 @@ def test_fullsize_delassus_apply(orc, R, shuffled):
     s = 1e-6
     y_ref = orc.delassus_apply(W, ia, ib, n, ta, tb, s, x)
     F_ref, U_ref = orc.wrench(W, ia, ib, n, ta, tb, x)
-    ctx = _ctx(R, dict(dynamics=0, dt=1e-3, cutoff=0.1, eps_ncp=1e-5, box=[0, 0, 0]))
+    ctx = _ctx(R, dict(dynamics=0, dt=1e-3, cutoff=0.1, eps_ncp=1e-5, box=[0, 0, 0]), layout=layout)
     bodies = R.BodyState.from_scene(b)
     cs = R.ConstraintStore.from_rows(ia, ib, n, ta, tb)
     ctx.prepare_operator(bodies, cs)
+    assert ctx.stats()["op_layout"] == layout
     xd = torch.as_tensor(x, device="cuda")
     yd = torch.empty_like(xd)
     ctx.delassus_apply(bodies, cs, xd, yd, s)
@@ -138,18 +140,20 @@ def test_fullsize_cfg5_step_invariants(orc, R, cfg5_full):
     assert np.max(np.abs(c["g"] - (Alam + c["q"]))) <= 1e-12 * np.max(np.abs(Alam))
 
 
-def test_fullsize_cfg5_solve_against_oracle_operator(orc, R, cfg5_full):
+@pytest.mark.parametrize("layout", [0, 1])
+def test_fullsize_cfg5_solve_against_oracle_operator(orc, R, cfg5_full, layout):
     """cfg5 A_0 (5.3M rows) solved in the bench's launch configuration (BB,
     3000-iteration cap, compact-row K7): the g the GPU returns equals the
     oracle's own s D^T W D lambda + q on EVERY row (1e-12 of the scale of
     A lambda), and the returned pair satisfies lambda >= 0 and the reported
     residual r = max |min(lambda, g)|."""
     sc = cfg5_full
-    ctx = _ctx(R, sc, lcp_tol=1e-8, lcp_max_iter=3000)
+    ctx = _ctx(R, sc, lcp_tol=1e-8, lcp_max_iter=3000, layout=layout)
     bodies = R.BodyState.from_scene(sc)
     cs = R.ConstraintStore(12 * sc["n"])
     ctx.generate_contacts(bodies, cs)
     rep = ctx.solve_lcp(bodies, cs)
+    assert ctx.stats()["jds_solves"] == layout
     c = cs.to_numpy()
     lam, g, q = c["lam"], c["g"], c["q"]
     assert np.all(lam >= 0)

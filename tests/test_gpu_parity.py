@@ -42,9 +42,11 @@ def _net(orc, nb, nc, seed, dynamics):
 
 # ------------------------------------------------------------ Delassus apply
 
+@pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("dynamics", [0, 1])
 @pytest.mark.parametrize("nb,nc", [(7, 1), (97, 1000), (2000, 9973), (5000, 40001)])
-def test_delassus_apply_parity(orc, R, dynamics, nb, nc):
+def test_delassus_apply_parity(orc, R, dynamics, nb, nc, layout):
+    """layout 0 (CSR) and 1 (JDS)."""
     b, ia, ib, n, ta, tb = _net(orc, nb, nc, 11 + nb, dynamics)
     b["dynamics"] = dynamics
     W = orc.body_W(b)
@@ -52,10 +54,11 @@ def test_delassus_apply_parity(orc, R, dynamics, nb, nc):
     x = rng.standard_normal(nc)
     s = 0.37
     y_ref = orc.delassus_apply(W, ia, ib, n, ta, tb, s, x)
-    ctx = _ctx(R, dict(dynamics=dynamics, dt=1e-3, cutoff=0.1, eps_ncp=1e-5, box=[0, 0, 0]))
+    ctx = _ctx(R, dict(dynamics=dynamics, dt=1e-3, cutoff=0.1, eps_ncp=1e-5, box=[0, 0, 0]), layout=layout)
     bodies = R.BodyState.from_scene(b)
     cs = R.ConstraintStore.from_rows(ia, ib, n, ta, tb, capacity=nc + 13)
     ctx.prepare_operator(bodies, cs)
+    assert ctx.stats()["op_layout"] == layout
     xd = torch.as_tensor(x, device="cuda")
     yd = torch.empty_like(xd)
     ctx.delassus_apply(bodies, cs, xd, yd, s)
@@ -121,6 +124,68 @@ def test_delassus_apply_hubs_and_empty_bodies(orc, R, shuffled, dynamics):
     assert np.all(U.cpu().numpy()[np.setdiff1d(np.arange(nb), np.concatenate([ia, ib]))] == 0)
 
 
+@pytest.mark.parametrize("dynamics", [0, 1])
+def test_jds_apply_hubs_and_empty_bodies(orc, R, dynamics):
+    """JDS layout: a hub with 700 a-side rows, a hub with 300 b-side
+    entries, a pair with 130 parallel rows, runs of bodies without rows, a
+    ragged last warp; rows t = r x n (the layout needs the compact rows)."""
+    rng = np.random.default_rng(43)
+    nb = 1000 + 37
+    ia = [np.zeros(700, int), rng.integers(0, 900, size=300)]
+    ib = [rng.integers(1, nb, size=700), np.full(300, 950)]
+    ia.append(np.full(130, 500)); ib.append(np.full(130, 900))
+    live = rng.choice(np.arange(1, nb), size=300, replace=False)
+    a = rng.choice(live, size=400); b = rng.choice(live, size=400)
+    keep = a != b
+    ia.append(a[keep]); ib.append(b[keep])
+    ia, ib = np.concatenate(ia), np.concatenate(ib)
+    keep = ia != ib
+    ia, ib = ia[keep], ib[keep]
+    lo, hi = np.minimum(ia, ib), np.maximum(ia, ib)
+    o = np.lexsort((hi, lo))
+    ia, ib = lo[o].astype(np.int32), hi[o].astype(np.int32)
+    nc = len(ia)
+    n = rng.normal(size=(nc, 3))
+    n /= np.linalg.norm(n, axis=1, keepdims=True)
+    ta = np.cross(rng.uniform(-1, 1, size=(nc, 3)), n)
+    tb = np.cross(rng.uniform(-1, 1, size=(nc, 3)), n)
+    b_ = scenes.suspension(nb, (1.0, 0.6, 0.4), 0.3, 5, dynamics=dynamics)
+    W = orc.body_W(b_)
+    x = rng.standard_normal(nc)
+    y_ref = orc.delassus_apply(W, ia, ib, n, ta, tb, 1.0, x)
+    F_ref, U_ref = orc.wrench(W, ia, ib, n, ta, tb, x)
+    ctx = _ctx(R, dict(dynamics=dynamics, dt=1e-3, cutoff=0.1, eps_ncp=1e-5, box=[0, 0, 0]), layout=1)
+    bodies = R.BodyState.from_scene(b_)
+    cs = R.ConstraintStore.from_rows(ia, ib, n, ta, tb)
+    ctx.prepare_operator(bodies, cs)
+    assert ctx.stats()["op_layout"] == 1
+    xd = torch.as_tensor(x, device="cuda")
+    yd = torch.empty_like(xd)
+    ctx.delassus_apply(bodies, cs, xd, yd, 1.0)
+    assert np.max(np.abs(yd.cpu().numpy() - y_ref)) <= 1e-12 * np.max(np.abs(y_ref))
+    F = torch.empty(nb, 6, dtype=torch.float64, device="cuda")
+    U = torch.empty_like(F)
+    ctx.wrench(bodies, cs, xd, F, U)
+    assert np.max(np.abs(F.cpu().numpy() - F_ref)) <= 1e-12 * np.max(np.abs(F_ref))
+    assert np.max(np.abs(U.cpu().numpy() - U_ref)) <= 1e-12 * np.max(np.abs(U_ref))
+    assert np.all(U.cpu().numpy()[np.setdiff1d(np.arange(nb), np.concatenate([ia, ib]))] == 0)
+    # the same solve on both layouts (q > 0 on the 130 parallel rows: they stay
+    # inactive, so the LCP keeps a well-conditioned active set)
+    qh = rng.standard_normal(nc) * 1e-3
+    qh[(ia == 500) & (ib == 900)] = 1e-3
+    q = torch.as_tensor(qh, device="cuda")
+    out = []
+    for lay in (0, 1):
+        c2 = _ctx(R, dict(dynamics=dynamics, dt=1e-3, cutoff=0.1, eps_ncp=1e-5, box=[0, 0, 0]), layout=lay,
+                  lcp_tol=1e-10, lcp_max_iter=2_000_000)
+        s2 = R.ConstraintStore.from_rows(ia, ib, n, ta, tb)
+        s2.q[:nc] = q
+        rep = c2.solve_lcp(bodies, s2)
+        assert rep["converged"] and c2.stats()["jds_solves"] == lay
+        out.append((s2.lam[:nc].cpu().numpy(), s2.g[:nc].cpu().numpy()))
+    assert np.max(np.abs(out[0][1] - out[1][1])) <= 1e-6 * np.max(np.abs(out[0][1])) + 1e-9
+
+
 def test_delassus_empty_and_state(orc, R):
     b, ia, ib, n, ta, tb = _net(orc, 10, 5, 3, 0)
     ctx = _ctx(R, dict(dynamics=0, dt=1e-3, cutoff=0.1, eps_ncp=1e-5, box=[0, 0, 0]))
@@ -148,15 +213,18 @@ def cfg1_a0(orc):
     return sc, r
 
 
+@pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("solver", [0, 1, 2])
-def test_lcp_solve_parity_cfg1(orc, R, cfg1_a0, solver):
+def test_lcp_solve_parity_cfg1(orc, R, cfg1_a0, solver, layout):
     sc, r = cfg1_a0
     c = r["constraints"]
-    ctx = _ctx(R, sc, lcp_tol=1e-10, solver=solver, lcp_max_iter=2_000_000)
+    ctx = _ctx(R, sc, lcp_tol=1e-10, solver=solver, lcp_max_iter=2_000_000, layout=layout)
     bodies = R.BodyState.from_scene(sc)
     cs = R.ConstraintStore.from_rows(c["ia"], c["ib"], c["n"], c["ta"], c["tb"], q=r["q_hist"][0])
     rep = ctx.solve_lcp(bodies, cs)
     assert rep["converged"] and rep["residual"] <= 1e-10
+    # JDS unless the fused APGD solver (CSR only)
+    assert ctx.stats()["jds_solves"] == (1 if layout == 1 and solver != 2 else 0)
     lam = cs.lam[:cs.count].cpu().numpy()
     g = cs.g[:cs.count].cpu().numpy()
     lam_ref, g_ref = c["lam"], r["g_hist"][0]
@@ -340,13 +408,13 @@ def _sorted_rows(ia, ib, gen):
     return np.lexsort((ib, ia, gen))
 
 
-def _compare_step(orc, R, sc, tol_cfg=1e-9, max_recursions=50, solver=0, reorder=1):
+def _compare_step(orc, R, sc, tol_cfg=1e-9, max_recursions=50, solver=0, reorder=1, layout=0):
     # Both sides solve every LCP to r <= 1e-12: two independent solvers that
     # each stop at r <= 1e-10 leave rotations differing by ~1e-9 (measured
     # 1.4e-9 on cfg1), at the edge of the 1e-9 configuration tolerance.
     r = orc.relcp_step(sc, lcp_tol=1e-12, max_recursions=max_recursions)
     ctx = _ctx(R, sc, lcp_tol=1e-12, max_recursions=max_recursions, lcp_max_iter=2_000_000, solver=solver,
-               reorder=reorder)
+               reorder=reorder, layout=layout)
     bodies = R.BodyState.from_scene(sc)
     cs = R.ConstraintStore(8 * max(1, len(r["constraints"]["ia"])) + 64)
     rep = ctx.step(bodies, cs)
@@ -380,15 +448,17 @@ def _compare_step(orc, R, sc, tol_cfg=1e-9, max_recursions=50, solver=0, reorder
     return r, rep, g
 
 
-def test_step_parity_cfg1(orc, R):
-    _compare_step(orc, R, scenes.cfg1())
+@pytest.mark.parametrize("layout", [0, 1])
+def test_step_parity_cfg1(orc, R, layout):
+    _compare_step(orc, R, scenes.cfg1(), layout=layout)
 
 
+@pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("solver", [1, 2])
-def test_step_parity_cfg1_apgd(orc, R, solver):
+def test_step_parity_cfg1_apgd(orc, R, solver, layout):
     """The whole step with APGD / fused APGD against the oracle's BB step
     (solution parity: every LCP solved to r <= 1e-12 on both sides)."""
-    _compare_step(orc, R, scenes.cfg1(), solver=solver)
+    _compare_step(orc, R, scenes.cfg1(), solver=solver, layout=layout)
 
 
 @pytest.mark.parametrize("reorder", [0, 2])
@@ -473,16 +543,18 @@ def test_step_parity_cfg1_bigdt(orc, R):
     assert rep["recursions"] >= 1 and rep["status"] == 0
 
 
-def test_step_parity_bigdt_augments(orc, R):
+@pytest.mark.parametrize("layout", [0, 1])
+def test_step_parity_bigdt_augments(orc, R, layout):
     sc = scenes.suspension(300, (1.0, 0.6, 0.4), 0.3, 9, dt=2e-2)
-    r, rep, _ = _compare_step(orc, R, sc, max_recursions=2)
+    r, rep, _ = _compare_step(orc, R, sc, max_recursions=2, layout=layout)
     assert rep["recursions"] >= 1
 
 
-def test_step_parity_cfg5_recipe(orc, R):
+@pytest.mark.parametrize("layout", [0, 1])
+def test_step_parity_cfg5_recipe(orc, R, layout):
     """cfg5 recipe (the bench workload) at 1000 bodies, two augmentations."""
     sc = scenes.cfg5(n=1000)
-    r, rep, _ = _compare_step(orc, R, sc, max_recursions=2)
+    r, rep, _ = _compare_step(orc, R, sc, max_recursions=2, layout=layout)
     assert rep["recursions"] == 2
 
 
@@ -527,9 +599,10 @@ def test_timing_mode_same_result(R, solver):
 
 # ------------------------------------------------------------ cfg3 / cfg4 recipes
 
+@pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("solver", [0, 1, 2])
 @pytest.mark.parametrize("c_fixed", [None, 3])
-def test_cfg4_network_lcp_parity(orc, R, c_fixed, solver):
+def test_cfg4_network_lcp_parity(orc, R, c_fixed, solver, layout):
     """Given chainmail network (cfg4 recipe, 16 x 16 rings): rows, q, and the
     solved LCP against the oracle.  c = 3 per link makes N_C exceed the free
     DOFs, so lambda is not unique: compare D lambda and g (Lemma 5, R13)."""
@@ -537,7 +610,7 @@ def test_cfg4_network_lcp_parity(orc, R, c_fixed, solver):
     # r <= 1e-12 on both sides: with 1-3 rows per link A is ill-conditioned and
     # r <= 1e-10 leaves lambda determined only to ~2e-6 relative (R19)
     x_ref, g_ref, info, W, rw = orc.network_lcp(sc, 1e-12)
-    ctx = _ctx(R, sc, lcp_tol=1e-12, lcp_max_iter=2_000_000, solver=solver)
+    ctx = _ctx(R, sc, lcp_tol=1e-12, lcp_max_iter=2_000_000, solver=solver, layout=layout)
     bodies = R.BodyState.from_scene(sc)
     net = sc["network"]
     cs = R.ConstraintStore(len(net["ia"]) + 7)

@@ -19,7 +19,8 @@ if len(sys.argv) > 3 and sys.argv[3] == "relaxed":
     pos, quat, _ = drivers.relax(sc, max_recursions=0, lcp_max_iter=20000, max_steps=60)
     sc = scenes.with_state(sc, pos.cpu().numpy(), quat.cpu().numpy(), 55, "cfg5-relaxed")
 ctx = R.Context(dynamics=sc["dynamics"], dt=sc["dt"], box=list(sc["box"]), lcp_max_iter=iters, lcp_tol=1e-30,
-                solver=int(os.environ.get("RELCP_SOLVER", "0")))  # 20 power iterations: APGD steps 1/(1.1 L)
+                solver=int(os.environ.get("RELCP_SOLVER", "0")),
+                layout=int(os.environ.get("RELCP_LAYOUT", "0")))  # 20 power iterations: APGD steps 1/(1.1 L)
 bodies = R.BodyState.from_scene(sc)
 cs = R.ConstraintStore(8 * n)
 ctx.generate_contacts(bodies, cs)
@@ -66,4 +67,6 @@ st = ctx.stats()
 it, sp = max(1, st["iter_timed"]), max(1, st["split_timed"])
 print(f"solve {rep['iterations']} it in {time.time() - t:.3f}s; scatter {st['scatter_ms'] / sp:.4f} ms "
       f"gather {st['gather_ms'] / sp:.4f} ms (first batch); iter {st['iter_ms'] / it:.4f} ms over {it}; iter alg "
-      f"{(216 * nc + 152 * n) / (st['iter_ms'] / it) / 1e6:.0f} GB/s", flush=True)
+      f"{(216 * nc + 152 * n) / (st['iter_ms'] / it) / 1e6:.0f} GB/s; K6 alg "
+      f"{(96 * nc + 104 * n) / (st['scatter_ms'] / sp) / 1e6:.0f} GB/s; layout {st['op_layout']} "
+      f"jds_solves {st['jds_solves']} resid {rep['residual']:.3e}", flush=True)
