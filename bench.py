@@ -69,6 +69,8 @@ def parse():
     ap.add_argument("--no-apply", action="store_true")
     ap.add_argument("--no-literal", action="store_true", help="skip the capped literal-cfg5 secondary line")
     ap.add_argument("--no-relabel", action="store_true", help="skip the relabelled-bodies secondary line")
+    ap.add_argument("--layout", type=int, default=None, help="operator layout (0 CSR, 1 JDS, 2 AUTO; default: the library's)")
+    ap.add_argument("--power-iters", type=int, default=None, help="power iterations per LCP (default: the library's)")
     return ap.parse_args()
 
 
@@ -349,9 +351,12 @@ def run_ours(args, rank, world, dist):
     cs = R.ConstraintStore(cap)
 
     # ---- headline: one complete Algorithm-1 step on cfg5-relaxed
+    lay = {} if args.layout is None else dict(layout=args.layout)
+    if args.power_iters is not None:
+        lay["power_iters"] = args.power_iters
     ctx = R.Context(dynamics=sc["dynamics"], dt=sc["dt"], box=list(sc["box"]), cutoff=sc["cutoff"],
                     eps_ncp=sc["eps_ncp"], lcp_tol=1e-8, lcp_max_iter=args.lcp_max_iter,
-                    max_recursions=args.max_recursions)
+                    max_recursions=args.max_recursions, **lay)
     bodies = R.BodyState.from_scene(sc)
     init = {k: getattr(bodies, k).clone() for k in ("pos", "quat", "vel")}
     ms, stats, reports, clk = time_steps(ctx, bodies, init, cs, args.steps, args.warmup, dist,
@@ -476,7 +481,7 @@ def run_ours(args, rank, world, dist):
                     n_bodies=args.n, max_recursions=args.max_recursions, lcp_max_iter=args.lcp_max_iter,
                     lcp_tol=1e-8, parallelism=f"replicas{world}", l2="inputs larger than L2 (GB working set)",
                     n_c=last.get("n_c"), lcp_iters=last.get("iterations"), n_pairs=last.get("n_pairs"),
-                    relaxation=relax_info),
+                    operator_layout=("JDS" if stats.get("op_layout") == 1 else "CSR"), relaxation=relax_info),
         complete_step=complete,
         roofline=dict(bound="hbm", kernel="LCP iteration (K6 scatter + K7 gather)", unit="GB/s", traffic=traffic,
                       traffic_n_c=traffic_nc, traffic_over_algorithmic=traffic_ratio, peak_source=peak_src, **roof),

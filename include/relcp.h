@@ -87,10 +87,13 @@ typedef struct relcp_params {
                              when fewer than RELCP_REORDER_COHERENT of the
                              consecutive caller bodies (b, b+1) lie in the same
                              or adjacent cells], _ON (see relcp_step)              */
-    int32_t layout;       /* operator layout of the LCP solve: RELCP_LAYOUT_CSR
-                             [default] | RELCP_LAYOUT_JDS (used when the store is
-                             sorted by ia and every row has t . n ~ 0; else
-                             CSR).  Results agree to rounding. */
+    int32_t layout;       /* operator layout of the LCP solve: RELCP_LAYOUT_CSR |
+                             RELCP_LAYOUT_JDS | RELCP_LAYOUT_AUTO [default: JDS
+                             for RELCP_LAYOUT_JDS_MIN_BODIES <= N and
+                             N_C <= RELCP_LAYOUT_JDS_MAX_ROWS, else CSR].  JDS
+                             needs a store sorted by ia and rows with
+                             t . n ~ 0 (else CSR).  Results agree to rounding
+                             (DESIGN.md §5). */
 } relcp_params;
 
 #define RELCP_REORDER_OFF 0
@@ -107,10 +110,15 @@ typedef struct relcp_params {
  * in that order (ids, compact rows, q, lambda, g) and writes lambda and g
  * back in the caller's row order; K6 streams whole columns and sums them
  * from shared memory without bank conflicts.  Measured equal in time to CSR
- * at cfg5 with ~20 % less DRAM traffic (profiles/README.md), hence not the
- * default.  The fused APGD solver always uses CSR.                         */
+ * at cfg5 and cfg4 (HBM-streaming stores: +-1 %), 12 % faster per iteration
+ * at cfg3 (431k rows, an L2-sized store), 45 % slower at cfg2 (20k bodies,
+ * skewed degrees), with ~20 % less DRAM traffic (profiles/README.md): AUTO
+ * picks JDS in the mid regime only.  The fused APGD solver always uses CSR. */
 #define RELCP_LAYOUT_CSR 0
 #define RELCP_LAYOUT_JDS 1
+#define RELCP_LAYOUT_AUTO 2
+#define RELCP_LAYOUT_JDS_MIN_BODIES 65536
+#define RELCP_LAYOUT_JDS_MAX_ROWS 2097152
 
 /* LCP solvers (the paper names only the family; reading R1):
  *   BB   Barzilai-Borwein projected gradient (alternating BB1 / BB2 steps);

@@ -33,7 +33,7 @@ static int check_params(const relcp_params *p) {
     if (p->solver != RELCP_SOLVER_BB && p->solver != RELCP_SOLVER_APGD && p->solver != RELCP_SOLVER_APGD_FUSED)
         return 0;
     if (p->reorder < RELCP_REORDER_OFF || p->reorder > RELCP_REORDER_ON) return 0;
-    if (p->layout != RELCP_LAYOUT_CSR && p->layout != RELCP_LAYOUT_JDS) return 0;
+    if (p->layout < RELCP_LAYOUT_CSR || p->layout > RELCP_LAYOUT_AUTO) return 0;
     return 1;
 }
 
@@ -407,7 +407,7 @@ void relcp_default_params(relcp_params *p) {
     p->xi = 1.0;
     p->n_dirs = 256;
     p->reorder = RELCP_REORDER_AUTO;
-    p->layout = RELCP_LAYOUT_CSR;
+    p->layout = RELCP_LAYOUT_AUTO;
 }
 
 int relcp_create(relcp_ctx **out, const relcp_params *p, void *cuda_stream) {

@@ -324,8 +324,10 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
     CK(cudaStreamSynchronize(ctx->stream));
     if (flags[0]) return set_err(ctx, RELCP_E_ARG, "prepare: body index out of range or ia == ib");
     ctx->op_compact = nc > 0 && !flags[1];
+    const int lay = ctx->p.layout;
     const bool jds = ctx->jds_enable && sorted && ctx->op_compact && ctx->p.solver != RELCP_SOLVER_APGD_FUSED &&
-                     ctx->p.layout == RELCP_LAYOUT_JDS;
+                     (lay == RELCP_LAYOUT_JDS || (lay == RELCP_LAYOUT_AUTO && nb >= RELCP_LAYOUT_JDS_MIN_BODIES &&
+                                                  nc <= RELCP_LAYOUT_JDS_MAX_ROWS));
     ctx->op_jds = jds;
     if (jds) CKS(op_prepare_jds(ctx, nb, nc, cs));
     const int64_t Ee = sorted ? nc : E;  // CSR entries: b-side only when sorted

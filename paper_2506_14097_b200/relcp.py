@@ -44,7 +44,7 @@ class Params(ctypes.Structure):
 
 SOLVER_BB, SOLVER_APGD, SOLVER_APGD_FUSED = 0, 1, 2
 REORDER_OFF, REORDER_AUTO, REORDER_ON = 0, 1, 2
-LAYOUT_CSR, LAYOUT_JDS = 0, 1
+LAYOUT_CSR, LAYOUT_JDS, LAYOUT_AUTO = 0, 1, 2
 
 
 class Bodies(ctypes.Structure):

@@ -63,10 +63,11 @@ def run(name):
     gen_s = time.time() - t0
     n = sc["n"]
     ctx = R.Context(dynamics=sc["dynamics"], dt=sc["dt"], box=list(sc["box"]), cutoff=sc["cutoff"],
-                    eps_ncp=sc["eps_ncp"], lcp_tol=1e-8, lcp_max_iter=3000, max_recursions=2 if name == "cfg5" else 50)
+                    eps_ncp=sc["eps_ncp"], lcp_tol=1e-8, lcp_max_iter=3000, max_recursions=2 if name == "cfg5" else 50,
+                    layout=int(os.environ.get("RELCP_LAYOUT", "2")))
     bodies = R.BodyState.from_scene(sc)
     init = {k: getattr(bodies, k).clone() for k in ("pos", "quat", "vel")}
-    out = dict(config=name, n_bodies=n, gen_s=gen_s)
+    out = dict(config=name, n_bodies=n, gen_s=gen_s, layout=int(os.environ.get("RELCP_LAYOUT", "2")))
     if name.startswith("cfg4"):
         net = sc["network"]
         cs = R.ConstraintStore(len(net["ia"]) + 16)
@@ -121,7 +122,7 @@ def run(name):
                lcp_iters=rep["iterations"], residuals=rep["residuals"], max_overlap=rep["max_overlap"],
                n_pairs=rep["n_pairs"], ms_generate=rep["ms_generate"], ms_solve=rep["ms_solve"],
                ms_check=rep["ms_check"], it_per_s_step=iters / (ms / 1e3),
-               iteration=dict(ms=it_ms / max(1, st["iter_timed"]),
+               iteration=dict(ms=st["iter_ms"] / max(1, st["iter_timed"]),
                               GBps=it_bytes / it_ms / 1e6 if it_ms > 0 else None,
                               frac_measured=it_bytes / it_ms / 1e6 / PEAK if it_ms > 0 else None),
                gpu_launches=st["launches"])
