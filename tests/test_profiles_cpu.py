@@ -13,8 +13,10 @@ P = os.path.join(ROOT, "profiles")
 
 def test_ncu_traffic_reproducible():
     out = subprocess.check_output([sys.executable, os.path.join(ROOT, "tools", "ncu_traffic.py"),
-                                   os.path.join(P, "r01_prof_iter_raw.csv"),
-                                   os.path.join(P, "r01_prof_apply_raw.csv")], cwd=ROOT, text=True)
+                                   os.path.join(P, "r02_prof_iter_relaxed_raw.csv"),
+                                   os.path.join(P, "r02_prof_apply_relaxed_raw.csv"),
+                                   "--nc", "7393149", "--n", "2000000", "--store", "cfg5-relaxed A_0"],
+                                  cwd=ROOT, text=True)
     got = json.loads(out)
     ref = json.load(open(os.path.join(P, "ncu_traffic.json")))
     for k in ("dram_bytes_per_iteration", "alg_bytes_per_iteration", "ratio", "apply_dram_bytes", "apply_ratio"):
@@ -22,7 +24,7 @@ def test_ncu_traffic_reproducible():
 
 
 def test_bench_line_has_contract_keys():
-    d = json.load(open(os.path.join(P, "r01_bench.json")))
+    d = json.load(open(os.path.join(P, "r02_bench.json")))
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
         assert k in d, k

@@ -46,11 +46,16 @@ for _ in range(3):
     ctx.delassus_apply(bodies, cs, x, y)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+prof_apply = os.environ.get("KBENCH_PROFILE_APPLY") == "1"  # ncu --profile-from-start off: only these applies
+if prof_apply:
+    torch.cuda.profiler.start()
 e0.record()
 for _ in range(20):
     ctx.delassus_apply(bodies, cs, x, y)
 e1.record()
 torch.cuda.synchronize()
+if prof_apply:
+    torch.cuda.profiler.stop()
 ms = e0.elapsed_time(e1) / 20
 print(f"N={n} N_C={nc} apply {ms:.4f} ms  alg {(176 * nc + 152 * n) / ms / 1e6:.0f} GB/s", flush=True)
 ctx.set_timing(True)
