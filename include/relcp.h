@@ -94,6 +94,11 @@ typedef struct relcp_params {
                              needs a store sorted by ia and rows with
                              t . n ~ 0 (else CSR).  Results agree to rounding
                              (DESIGN.md §5). */
+    int32_t cluster;      /* BB solves of small stores (N <= 8192 bodies,
+                             N_C <= 16384 rows, CSR layout) run the whole
+                             iteration loop in one 16-CTA thread-block cluster
+                             (DESIGN.md §5 "small stores") [1]; 0 = per-pass
+                             kernels.  Same iterates up to rounding.          */
 } relcp_params;
 
 #define RELCP_REORDER_OFF 0
@@ -346,7 +351,9 @@ int relcp_get_pairs(relcp_ctx *ctx, int32_t *pi, int32_t *pj, int64_t cap, int64
  *   jds_solves              LCP solves run on the JDS operator layout since
  *                           the reset (params.layout);
  *   op_layout               layout of the operator prepared last
- *                           (RELCP_LAYOUT_CSR or RELCP_LAYOUT_JDS). */
+ *                           (RELCP_LAYOUT_CSR or RELCP_LAYOUT_JDS);
+ *   cluster_solves          BB solves run by the single-cluster loop
+ *                           (params.cluster) since the reset. */
 typedef struct relcp_stats {
     int64_t launches;
     int64_t lcp_iterations;
@@ -359,6 +366,7 @@ typedef struct relcp_stats {
     int64_t jds_solves;
     int32_t op_layout;
     int32_t pad;
+    int64_t cluster_solves;
 } relcp_stats;
 int relcp_get_stats(relcp_ctx *ctx, relcp_stats *out);
 int relcp_reset_stats(relcp_ctx *ctx);

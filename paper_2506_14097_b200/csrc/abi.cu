@@ -408,6 +408,7 @@ void relcp_default_params(relcp_params *p) {
     p->n_dirs = 256;
     p->reorder = RELCP_REORDER_AUTO;
     p->layout = RELCP_LAYOUT_AUTO;
+    p->cluster = 1;
 }
 
 int relcp_create(relcp_ctx **out, const relcp_params *p, void *cuda_stream) {
@@ -713,6 +714,7 @@ int relcp_get_stats(relcp_ctx *ctx, relcp_stats *out) {
     out->jds_solves = ctx->jds_solves;
     out->op_layout = ctx->op_jds ? RELCP_LAYOUT_JDS : RELCP_LAYOUT_CSR;
     out->pad = 0;
+    out->cluster_solves = ctx->cluster_solves;
     return RELCP_OK;
 }
 
@@ -724,6 +726,7 @@ int relcp_reset_stats(relcp_ctx *ctx) {
     ctx->scatter_ms = ctx->gather_ms = ctx->iter_ms = 0.0;
     ctx->n_guard_total = 0;
     ctx->jds_solves = 0;
+    ctx->cluster_solves = 0;
     return RELCP_OK;
 }
 

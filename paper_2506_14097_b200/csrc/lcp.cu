@@ -18,6 +18,7 @@
 #include "reduce.cuh"
 
 #include "rows.cuh"
+#include "k6k7.cuh"
 // row . [U_a; U_b]: compact planes when the operator holds them (CR), else the store
 #define ROW_DOT(a) (CR ? row_dot_c((a), rs, ia, ib, rc, U) : row_dot_u((a), cap, ia, ib, n, ta, tb, U))
 #ifndef ITER_MINB
@@ -189,51 +190,15 @@ __global__ void __launch_bounds__(RELCP_NT, CR ? ITER_MINB_CR : ITER_MINB) k_lcp
     double *xw = st->par ? xA : xB, *gw = st->par ? gA : gB;  // the other slot: read (fix) then written
     double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t a_first = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const K7Rows r{nc, cap, rs, ia, ib, n, ta, tb, rc, q, s};
     // ILP constraints per thread per trip: independent loads in flight.  The
     // rare blended pass (fix) runs one row per trip to keep the register
     // budget of the common pass.
-    auto pass = [&](auto ilp_c, auto fix_c) {
-        constexpr int ILP = decltype(ilp_c)::value;
-        constexpr bool FIX = decltype(fix_c)::value;
-        for (int64_t a0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a0 < nc; a0 += ILP * stride) {
-            double xo[ILP], go[ILP], qv[ILP], rd[ILP];
-#pragma unroll
-            for (int u = 0; u < ILP; ++u) {
-                const int64_t a = a0 + u * stride;
-                const bool ok = a < nc;
-                const int64_t ac = ok ? a : a0;
-                xo[u] = xc[ac];
-                go[u] = gc[ac];
-                if (FIX) {  // current iterate = blend of the two slots
-                    const double xp = xw[ac], gp = gw[ac];
-                    xo[u] = fma(tl, xo[u] - xp, xp);
-                    go[u] = fma(tl, go[u] - gp, gp);
-                }
-                qv[u] = q[ac];
-                rd[u] = ROW_DOT(ac);
-            }
-#pragma unroll
-            for (int u = 0; u < ILP; ++u) {
-                const int64_t a = a0 + u * stride;
-                if (a >= nc) continue;
-                const double xn = fmax(0.0, xo[u] - alpha * go[u]);
-                const double gn = fma(s, rd[u], qv[u]);
-                xw[a] = xn;
-                gw[a] = gn;
-                const double sd = xn - xo[u], yd = gn - go[u];
-                acc[0] = fma(sd, sd, acc[0]);
-                acc[1] = fma(sd, yd, acc[1]);
-                acc[2] = fma(yd, yd, acc[2]);
-                acc[3] = fmax(acc[3], fabs(fmin(xn, gn)));
-                acc[4] = fmax(acc[4], isfinite(gn) ? 0.0 : 1.0);
-                acc[5] = fma(go[u], sd, acc[5]);
-            }
-        }
-    };
     if (fix)
-        pass(std::integral_constant<int, 1>{}, std::true_type{});
+        k7_rows<CR, 1, true>(a_first, stride, r, U, alpha, tl, xc, gc, xw, gw, acc);
     else
-        pass(std::integral_constant<int, CR ? ITER_ILP_CR : ITER_ILP>{}, std::false_type{});
+        k7_rows<CR, CR ? ITER_ILP_CR : ITER_ILP, false>(a_first, stride, r, U, alpha, tl, xc, gc, xw, gw, acc);
     const int ops[6] = {0, 0, 0, 1, 1, 0};
     if (grid_reduce_last<6>(acc, ops, part, counter, sh) && threadIdx.x == 0) {
         if (acc_out) {
@@ -367,6 +332,158 @@ static double op_scale(const relcp_ctx *ctx) {
     return ctx->p.dynamics == RELCP_INERTIAL ? dt * dt : dt;  // P:L553 vs P:L512
 }
 
+// ------------------------------------------------------------ small stores: one cluster runs the BB loop
+// Small stores are latency-bound: two kernels of dependent load chains plus a
+// grid-wide reduction, ~12 us per iteration at cfg1 against < 1 us of
+// traffic.  Here ONE thread-block
+// cluster of CL_CTAS CTAs (one per SM, non-portable size 16) runs `iters`
+// whole BB iterations per launch: K6 (k6_group) on the cluster's warps ->
+// cluster barrier -> K7 (k7_rows) -> each CTA's block partials into its own
+// shared memory -> cluster barrier -> every CTA combines the CTAs' partials
+// in rank order over distributed shared memory and runs the same finalize
+// (bb_iter_finalize) on its own copy of the LCP state, so all CTAs take
+// identical, deterministic steps with no third barrier (the next partials are
+// written only after the next K6 barrier).  Hardware cluster barriers replace
+// kernel boundaries and the grid's last-block reduction; U, x and g stay in
+// L2 (the store is a few MB).
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+#ifndef CL_CTAS
+#define CL_CTAS 16
+#endif
+#ifndef CL_NT
+#define CL_NT 512
+#endif
+#define CL_WARPS (CL_NT / 32)
+// eligibility: at most one 32-body group per warp of the cluster and a store
+// of <= 16k rows (cfg1: 11.8 -> 7.8 us per iteration; cfg2, 20k bodies / 31k
+// rows: 15.1 -> 19.3 us, because 16 SMs then run 2-3 dependent K6 chains per
+// warp where 148 SMs run one: the per-pass kernels stay above this size)
+#ifndef RELCP_CLUSTER_MAX_ROWS
+#define RELCP_CLUSTER_MAX_ROWS 16384
+#endif
+#define RELCP_CLUSTER_MAX_BODIES (CL_CTAS * CL_WARPS * 32)
+#ifndef CL_FENCE
+#define CL_FENCE 0  // extra gpu-scope fences before the cluster barriers (A/B)
+#endif
+#ifndef CL_ITERS
+#define CL_ITERS 128  // BB iterations per cluster launch (host convergence read between launches)
+#endif
+
+template <bool SORTED, bool CR>
+__global__ void __launch_bounds__(CL_NT, 1) k_bb_cluster(int iters, K6Op o, K7Rows r, double *xA, double *gA,
+                                                         double *xB, double *gB, double *U, LcpState *gst) {
+    extern __shared__ double2 cl_dyn[];  // CL_WARPS x 3 x (SCATTER_TILE + 1): K6 staging
+    __shared__ LcpState st;
+    __shared__ double part[6];
+    __shared__ double sh[6 * 32];
+    cg::cluster_group cl = cg::this_cluster();
+    const unsigned rank = cl.block_rank(), ncta = cl.num_blocks();
+    if (threadIdx.x == 0) st = *gst;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    auto c6 = reinterpret_cast<double2(*)[SCATTER_TILE + 1]>(cl_dyn + wl * 3 * (SCATTER_TILE + 1));
+    const int64_t nwarp = (o.nb + 31) >> 5;
+    const int ops[6] = {0, 0, 0, 1, 1, 0};
+    for (int it = 0; it < iters && !st.done; ++it) {
+        // K6: U = W D max(0, x - alpha g) (the current slot, or the blend after a shortened step)
+        const XEff xe = xeff_setup<1>(&st, xA, gA, xB, gB, nullptr);
+        for (int64_t w = rank * CL_WARPS + wl; w < nwarp; w += (int64_t)ncta * CL_WARPS)
+            k6_group<1, SORTED>(w, o, xe, c6, lane, U, nullptr, nullptr);
+        if (CL_FENCE) __threadfence();
+        cl.sync();  // barrier.cluster arrive (release) / wait (acquire): U visible to the cluster
+        // K7: x+, g+ into the other slot, partials
+        const bool par = st.par != 0;
+        const double *xc = par ? xB : xA, *gc = par ? gB : gA;
+        double *xw = par ? xA : xB, *gw = par ? gA : gB;
+        double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        const int64_t first = (int64_t)rank * CL_NT + threadIdx.x, stride = (int64_t)ncta * CL_NT;
+        if (st.fix)
+            k7_rows<CR, 1, true>(first, stride, r, U, st.alpha, st.t_ls, xc, gc, xw, gw, acc);
+        else
+            k7_rows<CR, 2, false>(first, stride, r, U, st.alpha, st.t_ls, xc, gc, xw, gw, acc);
+        block_reduce<6>(acc, ops, sh);
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int k = 0; k < 6; ++k) part[k] = acc[k];
+        if (CL_FENCE) __threadfence();
+        cl.sync();
+        if (threadIdx.x < 32) {
+            // lane q reads CTA q's partials (one DSMEM round trip), then a
+            // fixed shuffle tree: the same association in every CTA
+            const unsigned q = threadIdx.x;
+            double tot[6];
+            const double *pq = cl.map_shared_rank(part, q < ncta ? q : 0);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) tot[k] = q < ncta ? pq[k] : (ops[k] == 0 ? 0.0 : -INFINITY);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) tot[k] = ops[k] == 0 ? warp_sum(tot[k]) : warp_max(tot[k]);
+            if (threadIdx.x == 0) bb_iter_finalize(&st, tot);
+        }
+        __syncthreads();
+    }
+    if (rank == 0 && threadIdx.x == 0) *gst = st;
+    cl.sync();  // no CTA leaves while another may still read its partials
+}
+
+// 1 when the cluster launch of k_bb_cluster is possible on this device (probed once)
+static int cluster_probe(relcp_ctx *ctx) {
+    if (ctx->cl_ok >= 0) return ctx->cl_ok;
+    ctx->cl_ok = 0;
+    const size_t dyn = sizeof(double2) * CL_WARPS * 3 * (SCATTER_TILE + 1);
+    void (*ks[4])(int, K6Op, K7Rows, double *, double *, double *, double *, double *, LcpState *) = {
+        k_bb_cluster<true, true>, k_bb_cluster<true, false>, k_bb_cluster<false, true>, k_bb_cluster<false, false>};
+    for (auto k : ks) {
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL_CTAS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(CL_CTAS);
+    cfg.blockDim = dim3(CL_NT);
+    cfg.dynamicSmemBytes = dyn;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, (void *)k_bb_cluster<true, true>, &cfg) != cudaSuccess || ncl < 1) {
+        cudaGetLastError();
+        return 0;
+    }
+    ctx->cl_ok = 1;
+    return 1;
+}
+
+static int cluster_launch(relcp_ctx *ctx, int iters, bool sorted, bool cr, const K6Op &o, const K7Rows &r,
+                          double *xA, double *gA, double *xB, double *gB) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL_CTAS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(CL_CTAS);
+    cfg.blockDim = dim3(CL_NT);
+    cfg.dynamicSmemBytes = sizeof(double2) * CL_WARPS * 3 * (SCATTER_TILE + 1);
+    cfg.stream = ctx->stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    double *U = ctx->U.p;
+    LcpState *gst = ctx->st.p;
+    if (sorted && cr) CK(cudaLaunchKernelEx(&cfg, k_bb_cluster<true, true>, iters, o, r, xA, gA, xB, gB, U, gst));
+    else if (sorted) CK(cudaLaunchKernelEx(&cfg, k_bb_cluster<true, false>, iters, o, r, xA, gA, xB, gB, U, gst));
+    else if (cr) CK(cudaLaunchKernelEx(&cfg, k_bb_cluster<false, true>, iters, o, r, xA, gA, xB, gB, U, gst));
+    else CK(cudaLaunchKernelEx(&cfg, k_bb_cluster<false, false>, iters, o, r, xA, gA, xB, gB, U, gst));
+    ++ctx->launches;
+    return RELCP_OK;
+}
+
 // JDS layout: the solve's private slot-order view in / out
 __global__ void k_jds_in(int64_t nc, const int *__restrict__ perm, const double *__restrict__ lam,
                          const double *__restrict__ q, double *__restrict__ x, double *__restrict__ qs) {
@@ -498,6 +615,17 @@ static int lcp_solve_view(relcp_ctx *ctx, const relcp_bodies *b, relcp_constrain
             ctx->ev_ready = 1;
         }
     }
+    // small stores: the whole BB loop in one thread-block cluster (k_bb_cluster)
+    const bool use_cl = bb && !ctx->op_jds && nc <= RELCP_CLUSTER_MAX_ROWS && nb <= RELCP_CLUSTER_MAX_BODIES &&
+                        ctx->p.cluster != 0 && cluster_probe(ctx);
+    bool cl_timed = false;
+    K6Op k6o{};
+    K7Rows k7r{};
+    if (use_cl) {
+        k6o = op_k6(ctx);
+        k7r = K7Rows{nc, cs->capacity, ctx->op_rs, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->rc.p, cs->q, s};
+        ++ctx->cluster_solves;
+    }
     long long it_before = 0;
     int pending = 0, batches = 0;
     bool capturing = false, graph_timed = false;
@@ -547,7 +675,15 @@ static int lcp_solve_view(relcp_ctx *ctx, const relcp_bodies *b, relcp_constrain
         CK(cudaStreamSynchronize(st));
         const long long executed = ctx->st_host->iter - it_before;
         ctx->lcp_iterations += executed;
-        if (ctx->timing && pending > 0 && graph_timed) {
+        if (ctx->timing && pending > 0 && cl_timed) {
+            // a cluster launch stops at convergence: its time covers exactly the executed iterations
+            float a = 0.f;
+            CK(cudaEventElapsedTime(&a, ctx->ev[3 * 64], ctx->ev[3 * 64 + 1]));
+            if (executed > 0) {
+                ctx->iter_ms += a;
+                ctx->iter_timed += executed;
+            }
+        } else if (ctx->timing && pending > 0 && graph_timed) {
             // a graph batch counts only when every one of its iterations ran
             // (iterations after convergence exit at once and would dilute it)
             if (executed == pending) {
@@ -570,6 +706,15 @@ static int lcp_solve_view(relcp_ctx *ctx, const relcp_bodies *b, relcp_constrain
         }
         it_before = ctx->st_host->iter;
         if (ctx->st_host->done) break;
+        if (use_cl) {
+            if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * 64], st));
+            CKS(cluster_launch(ctx, CL_ITERS, ctx->op_sorted != 0, cr, k6o, k7r, cs->lambda, cs->g, xB, gB));
+            if (ctx->timing) CK(cudaEventRecord(ctx->ev[3 * 64 + 1], st));
+            cl_timed = true;
+            ++batches;
+            pending = CL_ITERS;
+            continue;
+        }
         if (!gexec && batches >= 1) {
             // the solve runs long: capture one batch as a CUDA graph, replay it
             cudaGraph_t graph = nullptr;

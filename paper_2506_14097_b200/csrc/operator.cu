@@ -28,12 +28,10 @@
 #include "common.cuh"
 #include "reduce.cuh"
 #include "rows.cuh"
+#include "k6k7.cuh"
 
 #ifndef SCATTER_WPB
 #define SCATTER_WPB 4    // warps per block (same-box A/B: 4 x 8 blocks beats 8 x 4)
-#endif
-#ifndef SCATTER_TILE
-#define SCATTER_TILE 64  // entries staged per warp per tile
 #endif
 #ifndef K6_REVERSE
 #define K6_REVERSE 1
@@ -362,9 +360,6 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
 // straight from the store planes; row_ptr / ecid / ew then hold only the
 // b-side entries (+[n; t_b]).  Otherwise row_ptr / ecid / ew hold both sides.
 // Per-body order: a-side rows, then CSR entries -- fixed, deterministic.
-struct V6 {
-    double v[6];
-};
 // the U / F transpose reuses a warp's staging area: 2 x 32 x 6 doubles
 static_assert(3 * (SCATTER_TILE + 1) * 2 >= 2 * 192, "SCATTER_TILE too small for the U/F staging");
 
@@ -373,152 +368,22 @@ static_assert(3 * (SCATTER_TILE + 1) * 2 >= 2 * 192, "SCATTER_TILE too small for
 // (x, g) / (x', g') are (x, g) / (xb, gb) or swapped by the device parity bit).
 template <int MODE, bool SORTED>
 __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
-    int64_t nb, int64_t E, const int *__restrict__ row_ptr, const int *__restrict__ ecid,
-    const double *__restrict__ ew, const int *__restrict__ pa, int64_t cap, const double *__restrict__ cn,
-    const double *__restrict__ cta, const double *__restrict__ x, const double *__restrict__ g,
-    const double *__restrict__ xb, const double *__restrict__ gb, const LcpState *__restrict__ st,
-    const double *__restrict__ xscale, const double *__restrict__ W, double *__restrict__ U,
-    double *__restrict__ Fout, const double *__restrict__ Fa) {
+    K6Op o, const double *__restrict__ x, const double *__restrict__ g, const double *__restrict__ xb,
+    const double *__restrict__ gb, const LcpState *__restrict__ st, const double *__restrict__ xscale,
+    double *__restrict__ U, double *__restrict__ Fout, const double *__restrict__ Fa) {
     // contributions staged as 3 planes of double2 (components 01, 23, 45):
     // 128-bit shared loads in the per-lane segment sums
     __shared__ double2 sm[SCATTER_WPB][3][SCATTER_TILE + 1];
-    double alpha = 0.0, beta = 0.0, tl = 1.0;
-    bool fix = false;
-    const double *xc = x, *gc = g, *xp = xb, *gp = gb;
-    if (MODE != 0) {
-        if (st->done) return;
-        alpha = st->alpha;
-    }
-    if (MODE == 1) {
-        // BB (lcp.cu k_lcp_iter): current slot by parity; after a shortened
-        // step the iterate is the blend xp + t (xc - xp) of the two slots
-        if (st->par) {
-            xc = xb; gc = gb; xp = x; gp = g;
-        }
-        fix = st->fix != 0;
-        tl = st->t_ls;
-    }
-    if (MODE == 2) {
-        beta = st->beta;
-        if (st->par) {
-            xc = xb; gc = gb; xp = x; gp = g;
-        }
-    }
-    if (MODE == 3 && st->par) xc = xb;  // fused BB: current iterate slot
-    const double sc = xscale ? *xscale : 1.0;
+    if (MODE != 0 && st->done) return;
+    const XEff xe = xeff_setup<MODE>(st, x, g, xb, gb, xscale);
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-    double2(*c6)[SCATTER_TILE + 1] = sm[wl];
-    const int64_t nwarp = (nb + 31) >> 5;
-    auto xeff = [&](int c) {
-        double xv;
-        if (MODE == 0 || MODE == 3) {
-            xv = xc[c];
-        } else if (MODE == 1) {
-            double x0 = xc[c], g0 = gc[c];
-            if (fix) {
-                const double xq = xp[c], gq = gp[c];
-                x0 = fma(tl, x0 - xq, xq);
-                g0 = fma(tl, g0 - gq, gq);
-            }
-            xv = fmax(0.0, x0 - alpha * g0);
-        } else {
-            const double x0 = xc[c], g0 = gc[c];
-            const double y = x0 + beta * (x0 - xp[c]), gy = g0 + beta * (g0 - gp[c]);
-            xv = fmax(0.0, y - alpha * gy);
-        }
-        return xv * sc;
-    };
+    const int64_t nwarp = (o.nb + 31) >> 5;
     for (int64_t wi = blockIdx.x * (int64_t)SCATTER_WPB + wl; wi < nwarp; wi += (int64_t)gridDim.x * SCATTER_WPB) {
         // K6_REVERSE: sweep bodies high -> low, so K6 starts on the rows, x and g
         // K7 (ascending) touched last (still in L2) and ends on the bodies whose
         // U / rows K7 touches first
         const int64_t w = K6_REVERSE ? nwarp - 1 - wi : wi;
-        const int64_t b0 = w << 5;
-        const int64_t b = b0 + lane;
-        const bool own = b < nb;
-        const int last = nb - b0 < 32 ? (int)(nb - b0 - 1) : 31;
-        double f[6] = {0, 0, 0, 0, 0, 0};
-        // stream [e0, e1) of the warp in coalesced tiles; lane sums its [s, t)
-        auto tiles = [&](int s, int t, auto &&fetch) {
-            const int e0 = __shfl_sync(0xffffffffu, s, 0);
-            const int e1 = __shfl_sync(0xffffffffu, t, last);
-            for (int base = e0; base < e1; base += SCATTER_TILE) {
-#pragma unroll
-                for (int i = 0; i < SCATTER_TILE / 32; ++i) {
-                    const int e = base + lane + 32 * i;
-                    if (e < e1) {  // slots past e1 are never read
-                        const V6 v = fetch(e);
-#pragma unroll
-                        for (int k = 0; k < 3; ++k) c6[k][lane + 32 * i] = make_double2(v.v[2 * k], v.v[2 * k + 1]);
-                    }
-                }
-                __syncwarp();
-                const int lo = max(s, base) - base, hi = min(t, base + SCATTER_TILE) - base;
-                for (int j = lo; j < hi; ++j)
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) {
-                        const double2 c = c6[k][j];
-                        f[2 * k] += c.x;
-                        f[2 * k + 1] += c.y;
-                    }
-                __syncwarp();
-            }
-        };
-        if (MODE == 3) {
-            // a-side sums were formed by the fused row pass (k_fused_rows)
-            if (own)
-#pragma unroll
-                for (int k = 0; k < 6; ++k) f[k] = Fa[k * nb + b];
-        } else if (SORTED) {
-            const int sa = own ? pa[b] : 0, ta_ = own ? pa[b + 1] : 0;
-            tiles(sa, ta_, [&](int e) {
-                const double xv = xeff(e);
-                V6 v;
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    v.v[k] = -cn[k * cap + e] * xv;
-                    v.v[3 + k] = -cta[k * cap + e] * xv;
-                }
-                return v;
-            });
-        }
-        const int s = own ? row_ptr[b] : 0, t = own ? row_ptr[b + 1] : 0;
-        tiles(s, t, [&](int e) {
-            const double xv = xeff(ecid[e]);
-            V6 v;
-#pragma unroll
-            for (int k = 0; k < 6; ++k) v.v[k] = ew[k * E + e] * xv;
-            return v;
-        });
-        // U_b = W_b F_b ; staged through shared memory for a coalesced AoS store
-        double u[6] = {0, 0, 0, 0, 0, 0};
-        if (own) {
-            const double w0 = W[b], s00 = W[nb + b], s01 = W[2 * nb + b], s02 = W[3 * nb + b], s11 = W[4 * nb + b],
-                         s12 = W[5 * nb + b], s22 = W[6 * nb + b];
-            u[0] = w0 * f[0];
-            u[1] = w0 * f[1];
-            u[2] = w0 * f[2];
-            u[3] = s00 * f[3] + s01 * f[4] + s02 * f[5];
-            u[4] = s01 * f[3] + s11 * f[4] + s12 * f[5];
-            u[5] = s02 * f[3] + s12 * f[4] + s22 * f[5];
-        }
-        double *flat = &c6[0][0].x;  // 3 * 65 double2 >= 2 * 192 doubles
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-            flat[6 * lane + k] = u[k];
-            flat[192 + 6 * lane + k] = f[k];
-        }
-        __syncwarp();
-        const int64_t nvals = 6 * (int64_t)(last + 1);
-#pragma unroll
-        for (int i = 0; i < 6; ++i) {
-            const int m = lane + 32 * i;
-            if (m < nvals) {
-                U[6 * b0 + m] = flat[m];
-                if (Fout) Fout[6 * b0 + m] = flat[192 + m];
-            }
-        }
-        __syncwarp();
+        k6_group<MODE, SORTED>(w, o, xe, sm[wl], lane, U, Fout, Fa);
     }
 }
 
@@ -707,6 +572,11 @@ __global__ void __launch_bounds__(32 * JDS_WPB, JT_MINB) k_scatter_jt(
     }
 }
 
+K6Op op_k6(const relcp_ctx *ctx) {
+    return K6Op{ctx->op_nb, ctx->op_sorted ? ctx->op_nc : 2 * ctx->op_nc, ctx->op_cap, ctx->row_ptr.p, ctx->ecid.p,
+                ctx->pa.p, ctx->ew.p, ctx->op_n, ctx->op_ta, ctx->W.p};
+}
+
 int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int mode, const double *xscale_dev,
                double *U, double *F, const double *xb, const double *gb, int slots) {
     if (ctx->op_jds) {
@@ -743,8 +613,8 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
     const int *pa = ctx->pa.p;
     const int64_t cap = ctx->op_cap;
     const double *cn = ctx->op_n, *cta = ctx->op_ta;
-#define SCATTER_ARGS nb, E, ctx->row_ptr.p, ctx->ecid.p, ctx->ew.p, pa, cap, cn, cta, x, g, xb, gb, ctx->st.p, \
-                     xscale_dev, ctx->W.p, U, F, ctx->Fa.p
+    const K6Op o{nb, E, cap, ctx->row_ptr.p, ctx->ecid.p, pa, ctx->ew.p, cn, cta, ctx->W.p};
+#define SCATTER_ARGS o, x, g, xb, gb, ctx->st.p, xscale_dev, U, F, ctx->Fa.p
     if (mode == 3) {
         if (!ctx->op_sorted) return set_err(ctx, RELCP_E_STATE, "fused solver needs a store sorted by ia");
         k_scatter<3, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);

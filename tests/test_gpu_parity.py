@@ -213,18 +213,23 @@ def cfg1_a0(orc):
     return sc, r
 
 
+@pytest.mark.parametrize("cluster", [0, 1])
 @pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("solver", [0, 1, 2])
-def test_lcp_solve_parity_cfg1(orc, R, cfg1_a0, solver, layout):
+def test_lcp_solve_parity_cfg1(orc, R, cfg1_a0, solver, layout, cluster):
+    """Every solver, both operator layouts, and for BB on the CSR layout the
+    single-cluster loop (cluster = 1, the default at this size) and the
+    per-pass kernels (cluster = 0)."""
     sc, r = cfg1_a0
     c = r["constraints"]
-    ctx = _ctx(R, sc, lcp_tol=1e-10, solver=solver, lcp_max_iter=2_000_000, layout=layout)
+    ctx = _ctx(R, sc, lcp_tol=1e-10, solver=solver, lcp_max_iter=2_000_000, layout=layout, cluster=cluster)
     bodies = R.BodyState.from_scene(sc)
     cs = R.ConstraintStore.from_rows(c["ia"], c["ib"], c["n"], c["ta"], c["tb"], q=r["q_hist"][0])
     rep = ctx.solve_lcp(bodies, cs)
     assert rep["converged"] and rep["residual"] <= 1e-10
-    # JDS unless the fused APGD solver (CSR only)
+    # JDS unless the fused APGD solver (CSR only); the cluster loop for BB on CSR
     assert ctx.stats()["jds_solves"] == (1 if layout == 1 and solver != 2 else 0)
+    assert ctx.stats()["cluster_solves"] == (1 if cluster and solver == 0 and layout == 0 else 0)
     lam = cs.lam[:cs.count].cpu().numpy()
     g = cs.g[:cs.count].cpu().numpy()
     lam_ref, g_ref = c["lam"], r["g_hist"][0]
@@ -408,13 +413,13 @@ def _sorted_rows(ia, ib, gen):
     return np.lexsort((ib, ia, gen))
 
 
-def _compare_step(orc, R, sc, tol_cfg=1e-9, max_recursions=50, solver=0, reorder=1, layout=0):
+def _compare_step(orc, R, sc, tol_cfg=1e-9, max_recursions=50, solver=0, reorder=1, layout=0, cluster=1):
     # Both sides solve every LCP to r <= 1e-12: two independent solvers that
     # each stop at r <= 1e-10 leave rotations differing by ~1e-9 (measured
     # 1.4e-9 on cfg1), at the edge of the 1e-9 configuration tolerance.
     r = orc.relcp_step(sc, lcp_tol=1e-12, max_recursions=max_recursions)
     ctx = _ctx(R, sc, lcp_tol=1e-12, max_recursions=max_recursions, lcp_max_iter=2_000_000, solver=solver,
-               reorder=reorder, layout=layout)
+               reorder=reorder, layout=layout, cluster=cluster)
     bodies = R.BodyState.from_scene(sc)
     cs = R.ConstraintStore(8 * max(1, len(r["constraints"]["ia"])) + 64)
     rep = ctx.step(bodies, cs)
@@ -550,11 +555,12 @@ def test_step_parity_bigdt_augments(orc, R, layout):
     assert rep["recursions"] >= 1
 
 
-@pytest.mark.parametrize("layout", [0, 1])
-def test_step_parity_cfg5_recipe(orc, R, layout):
-    """cfg5 recipe (the bench workload) at 1000 bodies, two augmentations."""
+@pytest.mark.parametrize("layout,cluster", [(0, 1), (1, 1), (0, 0)])
+def test_step_parity_cfg5_recipe(orc, R, layout, cluster):
+    """cfg5 recipe (the bench workload) at 1000 bodies, two augmentations;
+    CSR with the single-cluster BB loop (default), JDS, CSR per-pass kernels."""
     sc = scenes.cfg5(n=1000)
-    r, rep, _ = _compare_step(orc, R, sc, max_recursions=2, layout=layout)
+    r, rep, _ = _compare_step(orc, R, sc, max_recursions=2, layout=layout, cluster=cluster)
     assert rep["recursions"] == 2
 
 
@@ -570,15 +576,16 @@ def test_step_deterministic(R):
     assert all(torch.equal(a, b) for a, b in zip(out[0], out[1]))
 
 
-@pytest.mark.parametrize("solver", [0, 2])
-def test_timing_mode_same_result(R, solver):
+@pytest.mark.parametrize("solver,cluster", [(0, 0), (0, 1), (2, 0)])
+def test_timing_mode_same_result(R, solver, cluster):
     """relcp_set_timing only adds CUDA events (per kernel in the first batch,
-    around each CUDA-graph replay after it): the step is bitwise the one run
-    without timing, and the stats count the timed iterations."""
+    around each CUDA-graph replay after it; around each launch of the
+    single-cluster BB loop): the step is bitwise the one run without timing,
+    and the stats count the timed iterations."""
     sc = scenes.cfg1()
     out = []
     for timing in (False, True):
-        ctx = _ctx(R, sc, solver=solver, lcp_tol=1e-12)
+        ctx = _ctx(R, sc, solver=solver, lcp_tol=1e-12, cluster=cluster)
         bodies = R.BodyState.from_scene(sc)
         cs = R.ConstraintStore(8000)
         ctx.reset_stats()
@@ -588,7 +595,10 @@ def test_timing_mode_same_result(R, solver):
         out.append((bodies.pos.clone(), bodies.vel.clone(), cs.lam[:cs.count].clone()))
         iters = sum(rep["iterations"])
         assert st["lcp_iterations"] == iters
-        if timing:
+        assert (st["cluster_solves"] > 0) == (cluster == 1 and solver == 0)
+        if timing and st["cluster_solves"]:
+            assert st["split_timed"] == 0 and st["iter_timed"] == iters and st["iter_ms"] > 0
+        elif timing:
             assert iters > 64  # several batches: direct first batch + graph replays
             assert 0 < st["split_timed"] < st["iter_timed"] <= iters
             assert st["iter_ms"] >= st["scatter_ms"] + st["gather_ms"] - 1e-9 > 0
