@@ -99,6 +99,11 @@ typedef struct relcp_params {
                              iteration loop in one 16-CTA thread-block cluster
                              (DESIGN.md §5 "small stores") [1]; 0 = per-pass
                              kernels.  Same iterates up to rounding.          */
+    int32_t snsd_cert;    /* ellipsoid SNSD: accept a certified Newton maximum
+                             of an overlapping pair without the multistart
+                             when its depth is below half the smallest radius
+                             of curvature of A + B (curvature certificate,
+                             DESIGN.md R29) [1]; 0 = always multistart.      */
 } relcp_params;
 
 #define RELCP_REORDER_OFF 0
@@ -353,7 +358,10 @@ int relcp_get_pairs(relcp_ctx *ctx, int32_t *pi, int32_t *pj, int64_t cap, int64
  *   op_layout               layout of the operator prepared last
  *                           (RELCP_LAYOUT_CSR or RELCP_LAYOUT_JDS);
  *   cluster_solves          BB solves run by the single-cluster loop
- *                           (params.cluster) since the reset. */
+ *                           (params.cluster) since the reset;
+ *   snsd_multistart         ellipsoid pairs that went to the SNSD multistart
+ *                           (overlapping, not certified by R29) since the
+ *                           reset. */
 typedef struct relcp_stats {
     int64_t launches;
     int64_t lcp_iterations;
@@ -367,6 +375,7 @@ typedef struct relcp_stats {
     int32_t op_layout;
     int32_t pad;
     int64_t cluster_solves;
+    int64_t snsd_multistart;
 } relcp_stats;
 int relcp_get_stats(relcp_ctx *ctx, relcp_stats *out);
 int relcp_reset_stats(relcp_ctx *ctx);

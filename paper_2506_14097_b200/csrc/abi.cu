@@ -409,6 +409,7 @@ void relcp_default_params(relcp_params *p) {
     p->reorder = RELCP_REORDER_AUTO;
     p->layout = RELCP_LAYOUT_AUTO;
     p->cluster = 1;
+    p->snsd_cert = 1;
 }
 
 int relcp_create(relcp_ctx **out, const relcp_params *p, void *cuda_stream) {
@@ -715,6 +716,11 @@ int relcp_get_stats(relcp_ctx *ctx, relcp_stats *out) {
     out->op_layout = ctx->op_jds ? RELCP_LAYOUT_JDS : RELCP_LAYOUT_CSR;
     out->pad = 0;
     out->cluster_solves = ctx->cluster_solves;
+    long long nm = 0;
+    if (ctx->dstat.p && (cudaMemcpyAsync(&nm, ctx->dstat.p, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream) !=
+                             cudaSuccess || cudaStreamSynchronize(ctx->stream) != cudaSuccess))
+        return set_err(ctx, RELCP_E_CUDA, "stats: device counters");
+    out->snsd_multistart = nm;
     return RELCP_OK;
 }
 
@@ -727,6 +733,8 @@ int relcp_reset_stats(relcp_ctx *ctx) {
     ctx->n_guard_total = 0;
     ctx->jds_solves = 0;
     ctx->cluster_solves = 0;
+    if (ctx->dstat.p && cudaMemsetAsync(ctx->dstat.p, 0, 4 * sizeof(long long), ctx->stream) != cudaSuccess)
+        return set_err(ctx, RELCP_E_CUDA, "reset_stats: device counters");
     return RELCP_OK;
 }
 

@@ -260,10 +260,16 @@ __device__ __forceinline__ void write_out(const Eval &E, const double *nb, doubl
 // Phi >= F(d/|d|): if that bound is >= reject_above the pair cannot pass any
 // threshold below it (generation: cutoff; check: 0 > -eps) -> SNSD_BOUND.
 // Otherwise Newton from d/|d|; a maximum with F > 0 is global -> SNSD_OK /
-// SNSD_NONCONV; F <= 0 (overlap / touching) -> SNSD_MULTI (outputs hold the
-// Newton result as the incumbent for stage 2).
+// SNSD_NONCONV.  Overlap / touching (F <= 0): a certified critical point with
+// F > -cert is the global maximum (curvature certificate, R29: F(n) =
+// n.d - h_K(n) with K = A + B, whose radii of curvature are >= rho = r_min(A)
+// + r_min(B); by Blaschke's rolling theorem a ball of radius rho rolls freely
+// in K, so a critical point at depth |F| < rho is the unique nearest boundary
+// point of d, i.e. F = -dist(d, dK) = Phi; cert = rho / 2) -> SNSD_OK.
+// Otherwise SNSD_MULTI (outputs hold the Newton result as the incumbent for
+// the stage-2 multistart).
 __device__ int snsd_stage1(const double *d, const Sym &Sa, const Sym &Sb, double reject_above, double &phi,
-                           double *nout, double *ra, double *rb) {
+                           double *nout, double *ra, double *rb, double cert = 0.0) {
     const double dn = sqrt(d3(d, d));
     if (!(dn >= 1e-12)) {
         phi = nan("");
@@ -281,6 +287,7 @@ __device__ int snsd_stage1(const double *d, const Sym &Sa, const Sym &Sb, double
     feval(nb, d, Sa, Sb, Eb);
     write_out(Eb, nb, phi, nout, ra, rb);
     if (Eb.f > 0.0) return ok ? SNSD_OK : SNSD_NONCONV;
+    if (ok && Eb.f > -cert) return SNSD_OK;  // shallow overlap: the curvature certificate
     return ok ? SNSD_MULTI : -SNSD_MULTI;  // sign carries the incumbent's certification
 }
 
@@ -637,7 +644,7 @@ __global__ void __launch_bounds__(128, SNSD_MINB) k_snsd_stage1(const int *__res
                                                      Box3 box, double *__restrict__ phi, double *__restrict__ nrm,
                                                      double *__restrict__ ra, double *__restrict__ rb,
                                                      int *__restrict__ status, int64_t planes, int *multi,
-                                                     unsigned *n_multi) {
+                                                     unsigned *n_multi, const double *__restrict__ axes) {
     const int64_t m = *n_nlist;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = nlist[i];
@@ -645,8 +652,19 @@ __global__ void __launch_bounds__(128, SNSD_MINB) k_snsd_stage1(const int *__res
         Sym Sa, Sb;
         pair_geom(k, pi, pj, pos, Sig, box, d, Sa, Sb);
         double f, n[3], r1[3], r2[3];
+        // curvature certificate depth (R29): half the smallest radius of
+        // curvature of K = A + B; an ellipsoid's is min(e)^2 / max(e)
+        double cert = 0.0;
+        if (axes) {
+            auto rmin = [&](int64_t b) {
+                const double e0 = axes[3 * b], e1 = axes[3 * b + 1], e2 = axes[3 * b + 2];
+                const double lo = fmin(e0, fmin(e1, e2)), hi = fmax(e0, fmax(e1, e2));
+                return hi > 0.0 ? lo * lo / hi : 0.0;
+            };
+            cert = 0.5 * (rmin(pi[k]) + rmin(pj[k]));
+        }
         // reject_above = +inf: the bound was tested in stage 0
-        const int st = snsd_stage1(d, Sa, Sb, INFINITY, f, n, r1, r2);
+        const int st = snsd_stage1(d, Sa, Sb, INFINITY, f, n, r1, r2, cert);
         store_pair(k, planes, f, n, r1, r2, phi, nrm, ra, rb);
         const bool mult = st == SNSD_MULTI || st == -SNSD_MULTI;
         list_push(mult, k, multi, n_multi);
@@ -676,6 +694,8 @@ __global__ void __launch_bounds__(128, SNSD_MINB) k_snsd_stage2(const int *__res
         status[k] = st;
     }
 }
+
+__global__ void k_count_add(const unsigned *c, long long *acc) { *acc += *c; }
 
 int geo_snsd(relcp_ctx *ctx, int64_t np, const int *pi, const int *pj, const double *pos, const double *Sig,
              double *phi, double *nrm, double *ra, double *rb, int *status, int64_t planes, double reject_above,
@@ -708,10 +728,17 @@ int geo_snsd(relcp_ctx *ctx, int64_t np, const int *pi, const int *pj, const dou
                                                                    ctx->counter.p + 2, shape, axes);
     CKL();
     k_snsd_stage1<<<148 * 8, 128, 0, ctx->stream>>>(ctx->nlist.p, ctx->counter.p + 2, pi, pj, pos, Sig, bx, phi, nrm,
-                                                    ra, rb, status, planes, ctx->multi.p, ctx->counter.p + 1);
+                                                    ra, rb, status, planes, ctx->multi.p, ctx->counter.p + 1,
+                                                    ctx->p.snsd_cert ? axes : nullptr);
     CKL();
     k_snsd_stage2<<<148 * 8, 128, 0, ctx->stream>>>(ctx->multi.p, ctx->counter.p + 1, pi, pj, pos, Sig, bx, nd,
                                                     ctx->dirs.p, ctx->dirs32.p, phi, nrm, ra, rb, status, planes);
+    CKL();
+    if (!ctx->dstat.p) {
+        CK(ctx->dstat.grow(4));
+        CK(cudaMemsetAsync(ctx->dstat.p, 0, 4 * sizeof(long long), ctx->stream));
+    }
+    k_count_add<<<1, 1, 0, ctx->stream>>>(ctx->counter.p + 1, ctx->dstat.p);
     CKL();
     return RELCP_OK;
 }

@@ -39,7 +39,7 @@ class Params(ctypes.Structure):
     _fields_ = [("dynamics", i32), ("max_recursions", i32), ("dt", f64), ("eps_ncp", f64), ("cutoff", f64),
                 ("lcp_tol", f64), ("lcp_max_iter", i64), ("check_every", i32), ("power_iters", i32),
                 ("box", f64 * 3), ("xi", f64), ("n_dirs", i32), ("solver", i32), ("reorder", i32),
-                ("layout", i32), ("cluster", i32)]
+                ("layout", i32), ("cluster", i32), ("snsd_cert", i32)]
 
 
 SOLVER_BB, SOLVER_APGD, SOLVER_APGD_FUSED = 0, 1, 2
@@ -65,7 +65,8 @@ class SolveReport(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("launches", i64), ("lcp_iterations", i64), ("iter_timed", i64), ("scatter_ms", f64),
                 ("gather_ms", f64), ("split_timed", i64), ("iter_ms", f64), ("n_guard", i64),
-                ("jds_solves", i64), ("op_layout", i32), ("pad", i32), ("cluster_solves", i64)]
+                ("jds_solves", i64), ("op_layout", i32), ("pad", i32), ("cluster_solves", i64),
+                ("snsd_multistart", i64)]
 
 
 class StepReport(ctypes.Structure):
@@ -392,7 +393,7 @@ class Context:
         return dict(launches=st.launches, lcp_iterations=st.lcp_iterations, iter_timed=st.iter_timed,
                     scatter_ms=st.scatter_ms, gather_ms=st.gather_ms, split_timed=st.split_timed,
                     iter_ms=st.iter_ms, n_guard=st.n_guard, jds_solves=st.jds_solves, op_layout=st.op_layout,
-                    cluster_solves=st.cluster_solves)
+                    cluster_solves=st.cluster_solves, snsd_multistart=st.snsd_multistart)
 
     def reset_stats(self):
         self._check(self.L.relcp_reset_stats(self.h))

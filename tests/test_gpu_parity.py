@@ -350,6 +350,61 @@ def test_snsd_random_overlaps(orc, R):
     assert np.max(err) <= 1e-12, (np.argmax(err), phi[np.argmax(err)], phi_r[np.argmax(err)])
 
 
+def _quat_R(q):
+    s, x, y, z = (q / np.linalg.norm(q, axis=1, keepdims=True)).T
+    return np.stack([np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - s * z), 2 * (x * z + s * y)], -1),
+                     np.stack([2 * (x * y + s * z), 1 - 2 * (x * x + z * z), 2 * (y * z - s * x)], -1),
+                     np.stack([2 * (x * z - s * y), 2 * (y * z + s * x), 1 - 2 * (x * x + y * y)], -1)], 1)
+
+
+def test_snsd_curvature_certificate(orc, R):
+    """Shallow and medium overlaps (cfg5 and cfg2 shapes): with the curvature
+    certificate (R29) a certified Newton maximum at depth < rho / 2 (rho = the
+    sum of the two smallest radii of curvature, min(e)^2 / max(e) each) is
+    taken without the multistart.  Both settings equal the oracle's multistart
+    global maximum (Phi 1e-12 max(1, |d|), n 1e-10), the certificate removes
+    multistart work, and pairs deeper than rho / 2 still take the multistart."""
+    rng = np.random.default_rng(29)
+    m = 4000
+    quat = rng.standard_normal((2 * m, 4))
+    quat /= np.linalg.norm(quat, axis=1, keepdims=True)
+    r = rng.uniform(1, 4, size=2 * m)
+    axes = np.where((np.arange(2 * m) // 2 % 2 == 0)[:, None], np.array([1.0, 0.6, 0.4]),
+                    np.stack([np.ones(2 * m), 1 / r, 1 / r], 1))
+    u = rng.standard_normal((m, 3))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    Rm = _quat_R(quat)
+    Sig = np.einsum("bij,bj,bkj->bik", Rm, axes ** 2, Rm)
+    h = lambda S: np.sqrt(np.einsum("bi,bij,bj->b", u, S, u))
+    hs = h(Sig[0::2]) + h(Sig[1::2])
+    # |d| = (1 - delta)(h_a + h_b) along u: F(u) = -delta (h_a + h_b) <= Phi <= 0
+    delta = rng.uniform(0.0, 0.2, size=m)
+    pos = np.zeros((2 * m, 3))
+    pos[1::2] = u * ((1 - delta) * hs)[:, None]
+    pi = np.arange(0, 2 * m, 2, dtype=np.int32)
+    pj = pi + 1
+    phi_r, n_r, *_ = orc.snsd(pos, quat, axes, None, pi, pj)
+    rmin = lambda e: e.min(1) ** 2 / e.max(1)
+    rho = rmin(axes[0::2]) + rmin(axes[1::2])
+    shallow = (phi_r <= 0) & (-phi_r < 0.45 * rho)
+    assert shallow.sum() > 1000 and (-phi_r > 0.55 * rho).sum() > 100
+    dn = np.linalg.norm(pos[pj] - pos[pi], axis=1)
+    multi = []
+    for cert in (0, 1):
+        ctx = R.Context(dynamics=1, dt=1e-2, snsd_cert=cert)
+        bodies = R.BodyState(pos, quat, axes)
+        ctx.reset_stats()
+        phi, n, ra, rb, st = ctx.snsd_pairs(bodies, pi, pj)
+        multi.append(ctx.stats()["snsd_multistart"])
+        phi, n = phi.cpu().numpy(), n.cpu().numpy().T
+        err = np.abs(phi - phi_r) / np.maximum(1, dn)
+        assert np.max(err) <= 1e-12, (cert, np.argmax(err), phi[np.argmax(err)], phi_r[np.argmax(err)])
+        assert np.max(np.abs(n - n_r)) <= 1e-10
+    # a shallow pair whose ascent from d/|d| ends at another local maximum (value
+    # <= -rho, never the global one) still takes the multistart: allow 10 %
+    assert multi[0] >= (phi_r <= 0).sum() and multi[1] <= multi[0] - 0.9 * shallow.sum() and multi[1] > 0
+
+
 @pytest.mark.parametrize("n,phi_v", [(512, 0.3), (4000, 0.55), (20000, 0.55)])
 def test_broadphase_parity(orc, R, n, phi_v):
     sc = scenes.suspension(n, (1.0, 0.6, 0.4), phi_v, 3)

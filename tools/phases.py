@@ -3,7 +3,8 @@
 slightly slower step than bench.py's).  Build here (no GPU needed):
     python tools/phases.py --build
 then on the B200:
-    RELCP_LIB=paper_2506_14097_b200/lib/librelcp_phases.so python tools/phases.py [N]
+    RELCP_LIB=paper_2506_14097_b200/lib/librelcp_phases.so python tools/phases.py [N] [relaxed]
+("relaxed": the bench headline's cfg5-relaxed state and parameters)
 Prints the phase marks of the last of three steps, then a summary per phase."""
 import os
 import re
@@ -25,8 +26,15 @@ from paper_2506_14097_b200 import relcp as R  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 2_000_000
 sc = scenes.cfg5(n=n)
+relaxed = len(sys.argv) > 2 and sys.argv[2] == "relaxed"
+if relaxed:
+    from paper_2506_14097_b200 import drivers  # noqa: E402
+    import numpy as np  # noqa: E402
+    pos, quat, _ = drivers.relax(sc, max_recursions=0, lcp_max_iter=20000, max_steps=60)
+    sc = scenes.with_state(sc, pos.cpu().numpy(), quat.cpu().numpy(), 55, "cfg5-relaxed")
 ctx = R.Context(dynamics=sc["dynamics"], dt=sc["dt"], box=list(sc["box"]), cutoff=sc["cutoff"], eps_ncp=sc["eps_ncp"],
-                max_recursions=2, lcp_max_iter=3000, lcp_tol=1e-8)  # bench.py's parameters
+                max_recursions=50 if relaxed else 2, lcp_max_iter=200000 if relaxed else 3000,
+                lcp_tol=1e-8)  # bench.py's parameters (headline / literal line)
 bodies = R.BodyState.from_scene(sc)
 cs = R.ConstraintStore(8 * n)
 init = {k: getattr(bodies, k).clone() for k in ("pos", "quat", "vel")}
