@@ -616,6 +616,7 @@ static int step_core(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp
     double t1 = now_ms();
     R.ms_generate = t1 - t0;
     int recursion = 0;
+    ctx->L_reuse = 0.0;
     for (;;) {
         relcp_solve_report sr;
         double ts = now_ms();
@@ -625,6 +626,8 @@ static int step_core(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp
         PHASE(ctx, "solve.done");
         nvtxRangePop();
         R.ms_solve += now_ms() - ts;
+        ctx->L_reuse = rc < 0 ? 0.0 : sr.L;  // later recursions of this step may reuse it (R1)
+        ctx->L_reuse_nc = cs->count;
         if (rc < 0) return rc;
         if (rc == RELCP_W_MAX_ITER) warn = rc;
         R.n_c[recursion] = cs->count;
@@ -650,6 +653,7 @@ static int step_core(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp
         }
         ++recursion;
     }
+    ctx->L_reuse = 0.0;
     R.recursions = recursion;
     R.n_pairs = ctx->npairs;
     R.margin = ctx->margin;

@@ -327,6 +327,8 @@ __global__ void __launch_bounds__(RELCP_NT) k_objective(int64_t nc, const double
     }
 }
 
+__global__ void k_set_L(LcpState *st, double L) { st->L = L; }
+
 static double op_scale(const relcp_ctx *ctx) {
     const double dt = ctx->p.dt;
     return ctx->p.dynamics == RELCP_INERTIAL ? dt * dt : dt;  // P:L553 vs P:L512
@@ -555,10 +557,23 @@ static int lcp_solve_view(relcp_ctx *ctx, const relcp_bodies *b, relcp_constrain
     const int gridc = grid_for(nc, RELCP_NT, ITER_MINB);  // one wave of resident blocks
     k_project<<<gridc, RELCP_NT, 0, st>>>(nc, cs->lambda);
     CKL();
-    // power iteration for L = ||A|| (alpha_0 = 1/L, R1)
-    k_fill<<<gridc, RELCP_NT, 0, st>>>(nc, ctx->vtmp.p, 1.0);
-    CKL();
-    for (int it = 0; it < ctx->p.power_iters; ++it) {
+    // power iteration for L = ||A|| (alpha_0 = 1/L, R1).  A BB solve after an
+    // augmentation of <= 1 % of the rows in the same step reuses the previous
+    // L: the augmented A holds the previous one as a principal submatrix, so
+    // ||A|| can only grow, by little; BB's first step is then at most slightly
+    // long and the GLL line search guards it (R1).  APGD (step 1/(1.1 L))
+    // always recomputes.
+    const bool reuse_L = ctx->p.solver == RELCP_SOLVER_BB && ctx->L_reuse > 0.0 && isfinite(ctx->L_reuse) &&
+                         nc >= ctx->L_reuse_nc && (double)nc <= 1.01 * (double)ctx->L_reuse_nc;
+    if (reuse_L) {
+        k_set_L<<<1, 1, 0, st>>>(ctx->st.p, ctx->L_reuse);
+        CKL();
+    }
+    if (!reuse_L) {
+        k_fill<<<gridc, RELCP_NT, 0, st>>>(nc, ctx->vtmp.p, 1.0);
+        CKL();
+    }
+    for (int it = 0; it < (reuse_L ? 0 : ctx->p.power_iters); ++it) {
         CKS(op_scatter(ctx, nb, ctx->vtmp.p, nullptr, 0, &ctx->st.p->pnorm, ctx->U.p, nullptr, nullptr, nullptr, sl));
         CKS(op_gather_apply(ctx, cs, ctx->U.p, ctx->vtmp.p, s, 1));
     }
