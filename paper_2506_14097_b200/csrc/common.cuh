@@ -189,6 +189,8 @@ struct relcp_ctx {
     DevBuf<long long> scan_tmp;
     DevBuf<int> cell_count, cell_start, cell_fill, cell_items, body_cell;
     DevBuf<long long> pair_cnt;  // per body pair counts (then offsets)
+    int bp_cap = 0;              // slot-row capacity of the single-pass broadphase (0: two-pass)
+    DevBuf<int> bp_tmp;          // (nb, bp_cap) slot rows
     DevBuf<double> red;          // small reduction buffer
     double *red_host = nullptr;  // pinned (64 doubles)
     int64_t snsd_nonconv_total = 0;

@@ -862,6 +862,84 @@ __global__ void __launch_bounds__(128) k_pairs2(int64_t nb, const double *__rest
     }
 }
 
+// Single pass (the common case): each body's partners j > i go to a
+// fixed-capacity slot row tmp[i * cap ...] (sorted there), the count to
+// cnt[i]; a body with more than `cap` partners sets *ovf and the caller reruns
+// the two-pass kernel above.  cap comes from the previous broadphase's
+// largest per-body count (ctx->bp_cap), so the neighbour search runs once.
+__global__ void __launch_bounds__(128) k_pairs_one(int64_t nb, const double *__restrict__ pos,
+                                                   const double *__restrict__ rad, Grid G, double margin,
+                                                   const int *__restrict__ body_cell, const int *__restrict__ cell_start,
+                                                   const int *__restrict__ cell_count, const int *__restrict__ items,
+                                                   long long *__restrict__ cnt, int *__restrict__ tmp, int cap,
+                                                   int *__restrict__ ovf) {
+    for (int64_t ib = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ib < nb; ib += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)ib;
+        const int c = body_cell[i];
+        const int cx = c % G.nc[0], cy = (c / G.nc[0]) % G.nc[1], cz = c / (G.nc[0] * G.nc[1]);
+        int nx[3], ny[3], nz[3];
+        const int mx = axis_neighbours(cx, 0, G, nx), my = axis_neighbours(cy, 1, G, ny),
+                  mz = axis_neighbours(cz, 2, G, nz);
+        int *row = tmp + (int64_t)i * cap;
+        long long m = 0;
+        for (int a = 0; a < mz; ++a)
+            for (int b2 = 0; b2 < my; ++b2)
+                for (int e = 0; e < mx; ++e) {
+                    const int cc = (nz[a] * G.nc[1] + ny[b2]) * G.nc[0] + nx[e];
+                    const int s = cell_start[cc], t = s + cell_count[cc];
+                    for (int q = s; q < t; ++q) {
+                        const int j = items[q];
+                        if (j <= i) continue;
+                        if (!near_pair(pos, rad, G, margin, i, j)) continue;
+                        if (m < cap) row[m] = j;
+                        ++m;
+                    }
+                }
+        cnt[i] = m;
+        if (m > cap) {
+            *ovf = 1;
+            continue;
+        }
+        for (long long u = 1; u < m; ++u) {  // lexicographic (i, j) order
+            const int k = row[u];
+            long long v = u - 1;
+            while (v >= 0 && row[v] > k) {
+                row[v + 1] = row[v];
+                --v;
+            }
+            row[v + 1] = k;
+        }
+    }
+}
+
+__global__ void k_max_count(int64_t nb, const long long *__restrict__ cnt, int *mx) {
+    int m = 0;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, (int)min(cnt[b], (long long)1 << 30));
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
+}
+
+// slot rows -> the packed pair list at the scanned offsets
+__global__ void k_pairs_pack(int64_t nb, const long long *__restrict__ off, const int *__restrict__ tmp, int cap,
+                             int *__restrict__ pi, int *__restrict__ pj) {
+    const int64_t nw = (nb + 31) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        // a warp packs 32 consecutive bodies' rows, one body after the other
+        const int64_t b0 = w << 5;
+        const int64_t bl = b0 + 32 < nb ? b0 + 32 : nb;
+        for (int64_t i = b0; i < bl; ++i) {
+            const long long o = off[i], m = off[i + 1] - o;
+            for (long long u = lane; u < m; u += 32) {
+                pi[o + u] = (int)i;
+                pj[o + u] = tmp[i * cap + u];
+            }
+        }
+    }
+}
+
 // bounds: min pos (3), max pos (3), max rad
 __global__ void __launch_bounds__(RELCP_NT) k_bounds(int64_t nb, const double *__restrict__ pos,
                                                      const double *__restrict__ rad, double *part,
@@ -934,19 +1012,53 @@ int geo_broadphase(relcp_ctx *ctx, int64_t nb, const double *pos, const double *
     CKL();
     PHASE(ctx, "bp.cells");
     const int gp = grid_for(nb, 128, 32);
+    long long total = 0;
+    CK(ctx->scan_ll.grow(nb + 1));
+    if (ctx->bp_cap > 0 && (double)ctx->bp_cap * (double)nb <= 2.0e9) {
+        // one neighbour search into slot rows of the last search's largest count (+ slack)
+        const int cap = ctx->bp_cap;
+        CK(ctx->bp_tmp.grow((size_t)cap * nb));
+        CK(cudaMemsetAsync(ctx->counter.p + 3, 0, sizeof(unsigned), st));
+        k_pairs_one<<<gp, 128, 0, st>>>(nb, pos, rad, G, margin, ctx->body_cell.p, ctx->cell_start.p,
+                                        ctx->cell_count.p, ctx->cell_items.p, ctx->pair_cnt.p, ctx->bp_tmp.p, cap,
+                                        (int *)(ctx->counter.p + 3));
+        CKL();
+        CK(cudaMemsetAsync(ctx->pair_cnt.p + nb, 0, sizeof(long long), st));
+        CKS(scan_exclusive_ll(ctx, ctx->pair_cnt.p, ctx->scan_ll.p, nb + 1, &total));  // synchronises
+        int ovf = 0;
+        CK(cudaMemcpyAsync(&ovf, ctx->counter.p + 3, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (!ovf) {
+            PHASE(ctx, "bp.count_scan");
+            CK(ctx->pi.grow(total > 0 ? total : 1));
+            CK(ctx->pj.grow(total > 0 ? total : 1));
+            k_pairs_pack<<<grid_for(32 * ((nb + 31) / 32), 256, 8), 256, 0, st>>>(nb, ctx->scan_ll.p, ctx->bp_tmp.p,
+                                                                               cap, ctx->pi.p, ctx->pj.p);
+            CKL();
+            ctx->npairs = total;
+            PHASE(ctx, "bp.pairs");
+            return RELCP_OK;
+        }
+    }
     k_pairs2<0><<<gp, 128, 0, st>>>(nb, pos, rad, G, margin, ctx->body_cell.p, ctx->cell_start.p, ctx->cell_count.p,
                                     ctx->cell_items.p, ctx->pair_cnt.p, nullptr, nullptr);
     CKL();
     CK(cudaMemsetAsync(ctx->pair_cnt.p + nb, 0, sizeof(long long), st));
-    long long total = 0;
-    CK(ctx->scan_ll.grow(nb + 1));
     CKS(scan_exclusive_ll(ctx, ctx->pair_cnt.p, ctx->scan_ll.p, nb + 1, &total));
     PHASE(ctx, "bp.count_scan");
+    // the largest per-body count sizes the next search's slot rows (+ 25 % + 8 slack)
+    CK(cudaMemsetAsync(ctx->counter.p + 3, 0, sizeof(unsigned), st));
+    k_max_count<<<grid_for(nb), RELCP_NT, 0, st>>>(nb, ctx->pair_cnt.p, (int *)(ctx->counter.p + 3));
+    CKL();
     CK(ctx->pi.grow(total > 0 ? total : 1));
     CK(ctx->pj.grow(total > 0 ? total : 1));
     k_pairs2<1><<<gp, 128, 0, st>>>(nb, pos, rad, G, margin, ctx->body_cell.p, ctx->cell_start.p, ctx->cell_count.p,
                                     ctx->cell_items.p, ctx->scan_ll.p, ctx->pi.p, ctx->pj.p);
     CKL();
+    int mx = 0;
+    CK(cudaMemcpyAsync(&mx, ctx->counter.p + 3, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ctx->bp_cap = mx + mx / 4 + 8;
     ctx->npairs = total;
     PHASE(ctx, "bp.pairs");
     return RELCP_OK;
