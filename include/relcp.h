@@ -441,6 +441,16 @@ int relcp_dd_get_u(relcp_dd *dd, double *U);
 /* relcp_solve_lcp over the parts (BB, same parameters); cs = the loaded store.
  * Returns OK, W_MAX_ITER or E_NAN like relcp_solve_lcp.  Synchronises. */
 int relcp_dd_solve_lcp(relcp_dd *dd, relcp_constraints *cs, relcp_solve_report *rep);
+/* One ReLCP step (Algorithm 1; same contract, report and codes as
+ * relcp_step, in the caller's body order) whose LCP solves are the
+ * domain-decomposed BB solve above on each recursion's store; generation,
+ * checks and augmentation are replicated on every rank (every rank passes
+ * all bodies and the whole store; the single-domain kernels are
+ * deterministic, so every rank holds the same store).  NCCL: after each solve
+ * the ranks exchange their rows' lambda and g (grouped send / recv).
+ * DESIGN.md §8. */
+int relcp_dd_step(relcp_dd *dd, relcp_bodies *bodies, const double *f_ext, relcp_constraints *cs,
+                  relcp_step_report *rep);
 
 #ifdef __cplusplus
 }

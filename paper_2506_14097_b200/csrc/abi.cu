@@ -593,7 +593,7 @@ int relcp_check_and_augment(relcp_ctx *ctx, const relcp_bodies *Ck, relcp_constr
 // Algorithm 1 on one body labelling; relcp_step wraps it with the
 // internal body order (order.cu)
 static int step_core(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_constraints *cs,
-                     relcp_step_report *rep) {
+                     relcp_step_report *rep, relcp_solve_cb solve = nullptr, void *user = nullptr) {
     relcp_step_report R;
     memset(&R, 0, sizeof(R));
     const int64_t nb = b->n;
@@ -622,7 +622,7 @@ static int step_core(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp
         double ts = now_ms();
         nvtxRangePushA("relcp_solve_lcp");
         PHASE(ctx, "solve.enter");
-        rc = lcp_solve(ctx, b, cs, &sr);  // lines 3 / 10
+        rc = solve ? solve(user, ctx, b, cs, &sr) : lcp_solve(ctx, b, cs, &sr);  // lines 3 / 10
         PHASE(ctx, "solve.done");
         nvtxRangePop();
         R.ms_solve += now_ms() - ts;
@@ -670,6 +670,17 @@ static int step_core(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp
     if (rep) *rep = R;
     if (R.status) return R.status;
     return warn > 0 ? warn : RELCP_OK;
+}
+
+// Algorithm 1 in the caller's body order with another LCP solver (the
+// domain-decomposed solve, dd.cu relcp_dd_step)
+int step_entry(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_constraints *cs, relcp_step_report *rep,
+               relcp_solve_cb solve, void *user) {
+    CKS(check_views(ctx, b, cs));
+    if (!cs->g) return set_err(ctx, RELCP_E_ARG, "step: constraints.g is required");
+    if (ctx->p.dynamics == RELCP_INERTIAL && !b->vel) return set_err(ctx, RELCP_E_ARG, "step: inertial needs vel");
+    ctx->pairs_internal = 0;
+    return step_core(ctx, b, f_ext, cs, rep, solve, user);
 }
 
 extern "C" {

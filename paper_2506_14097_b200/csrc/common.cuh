@@ -271,6 +271,12 @@ int store_merge_appended(relcp_ctx *ctx, relcp_constraints *cs, int64_t n_old, i
 int store_is_sorted_by_ia(relcp_ctx *ctx, const relcp_constraints *cs, int *sorted_host);
 // lcp.cu
 int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relcp_solve_report *rep);
+// abi.cu: Algorithm 1 (relcp_step without the internal body order) with the LCP
+// solves delegated to `solve` (dd.cu relcp_dd_step)
+typedef int (*relcp_solve_cb)(void *user, relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs,
+                              relcp_solve_report *rep);
+int step_entry(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_constraints *cs, relcp_step_report *rep,
+               relcp_solve_cb solve, void *user);
 // split-reduction pieces of the BB solve for the domain-decomposed solve (dd.cu):
 // each writes its part's block-reduced partials to acc_out (device) instead of
 // finalizing; lcp_dd_finalize applies the finalize step of `kind` to ctx->st

@@ -188,6 +188,7 @@ struct relcp_dd {
     DevBuf<double> xB, gB, vtmp;
     dd_nccl_comm comm = nullptr;
     int64_t iterations = 0;
+    std::vector<int64_t> roff;  // (K + 1) row range of every part in the loaded store
 };
 
 __global__ void k_dd_gather_bodies(int64_t n, const int64_t *__restrict__ gid, const double *quat,
@@ -477,6 +478,10 @@ extern "C" int relcp_dd_load(relcp_dd *dd, const relcp_bodies *b, const relcp_co
         CK(cudaStreamSynchronize(ctx->stream));
     }
     dd_free(dd);
+    dd->roff.assign(dd->K + 1, nc);
+    for (int k = 0; k <= dd->K; ++k)  // rows sorted by ia: part k owns [roff[k], roff[k+1])
+        dd->roff[k] = std::lower_bound(ia.begin(), ia.end(), (int32_t)std::min<int64_t>(dd->off[k], INT32_MAX)) -
+                      ia.begin();
     for (int k = 0; k < dd->K; ++k) {
         if (dd->rank >= 0 && k != dd->rank) continue;
         DDPart *P = new DDPart();
@@ -707,4 +712,51 @@ extern "C" int relcp_dd_solve_lcp(relcp_dd *dd, relcp_constraints *cs, relcp_sol
     }
     if (h->nan) return set_err(ctx, RELCP_E_NAN, "dd solve: non-finite iterate after %lld iterations", h->iter);
     return h->conv ? RELCP_OK : RELCP_W_MAX_ITER;
+}
+
+// ------------------------------------------------------------ domain-decomposed ReLCP step
+// Algorithm 1 with every LCP solve distributed (relcp_dd_solve_lcp
+// on the store of the current recursion) and generation / checks / augmentation
+// replicated on every rank (each rank holds all body states; the step's
+// bitwise-deterministic single-domain kernels give every rank the same
+// store).  NCCL: after each solve every rank sends its rows' lambda and g to
+// every other rank (grouped send / recv), so the replicated check sees the
+// whole solution.
+static int dd_allgather_rows(relcp_dd *dd, relcp_constraints *cs) {
+    DDCTX;
+    if (dd->rank < 0 || dd->K == 1) return RELCP_OK;
+    const int me = dd->rank;
+    const int64_t m0 = dd->roff[me], mm = dd->roff[me + 1] - m0;
+    for (double *v : {cs->lambda, cs->g}) {
+        CKS(nccl_check(dd, g_nccl.GroupStart(), "ncclGroupStart"));
+        for (int q = 0; q < dd->K; ++q) {
+            if (q == me) continue;
+            if (mm) CKS(nccl_check(dd, g_nccl.Send(v + m0, mm, ncclDouble_, q, dd->comm, ctx->stream), "ncclSend"));
+            const int64_t r0 = dd->roff[q], rm = dd->roff[q + 1] - r0;
+            if (rm) CKS(nccl_check(dd, g_nccl.Recv(v + r0, rm, ncclDouble_, q, dd->comm, ctx->stream), "ncclRecv"));
+        }
+        CKS(nccl_check(dd, g_nccl.GroupEnd(), "ncclGroupEnd"));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    return RELCP_OK;
+}
+
+static int dd_step_solve(void *user, relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs,
+                         relcp_solve_report *rep) {
+    relcp_dd *dd = (relcp_dd *)user;
+    (void)ctx;
+    int rc = relcp_dd_load(dd, b, cs);
+    if (rc < 0) return rc;
+    rc = relcp_dd_solve_lcp(dd, cs, rep);
+    if (rc < 0) return rc;
+    const int rg = dd_allgather_rows(dd, cs);
+    return rg < 0 ? rg : rc;
+}
+
+extern "C" int relcp_dd_step(relcp_dd *dd, relcp_bodies *b, const double *f_ext, relcp_constraints *cs,
+                             relcp_step_report *rep) {
+    if (!dd) return RELCP_E_ARG;
+    DDCTX;
+    if (!b || dd->off[dd->K] != b->n) return set_err(ctx, RELCP_E_ARG, "dd_step: part offsets must end at n bodies");
+    return step_entry(ctx, b, f_ext, cs, rep, dd_step_solve, dd);
 }

@@ -29,7 +29,7 @@ EXPORTS = ["relcp_default_params", "relcp_create", "relcp_destroy", "relcp_last_
            "relcp_get_stats", "relcp_reset_stats", "relcp_set_timing", "relcp_load_constraints",
            "relcp_dd_plan_host", "relcp_dd_nccl_unique_id", "relcp_dd_create", "relcp_dd_destroy",
            "relcp_dd_last_error", "relcp_dd_load", "relcp_dd_info_get", "relcp_dd_delassus_apply", "relcp_dd_get_u",
-           "relcp_dd_solve_lcp"]
+           "relcp_dd_solve_lcp", "relcp_dd_step"]
 
 P = ctypes.c_void_p
 i32, i64, f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
@@ -145,6 +145,7 @@ def load(build_if_missing: bool = True):
     L.relcp_dd_delassus_apply.argtypes = [P, P, P, f64]
     L.relcp_dd_get_u.argtypes = [P, P]
     L.relcp_dd_solve_lcp.argtypes = [P, ctypes.POINTER(Constraints), ctypes.POINTER(SolveReport)]
+    L.relcp_dd_step.argtypes = [P, ctypes.POINTER(Bodies), P, ctypes.POINTER(Constraints), ctypes.POINTER(StepReport)]
     for name in EXPORTS:
         if name not in ("relcp_default_params", "relcp_last_error", "relcp_dd_last_error"):
             getattr(L, name).restype = ctypes.c_int
@@ -520,6 +521,18 @@ class DomainDecomposition:
     def get_u(self, U: torch.Tensor):
         n = int(self._views[0].n)
         self._check(self.L.relcp_dd_get_u(self.h, _dptr(U, torch.float64, 6 * n, "U")))
+
+    def step(self, bodies: BodyState, cs: ConstraintStore, f_ext: torch.Tensor | None = None):
+        """relcp_dd_step: Algorithm 1 with domain-decomposed LCP solves."""
+        bv, cv = bodies.view(), cs.view()
+        rep = StepReport()
+        fe = _dptr(f_ext, torch.float64, 6 * bodies.n, "f_ext", True)
+        rc = self.L.relcp_dd_step(self.h, ctypes.byref(bv), fe, ctypes.byref(cv), ctypes.byref(rep))
+        cs.sync_from(cv)
+        self._check(rc)
+        d = rep.as_dict()
+        d["rc"] = rc
+        return d
 
     def solve_lcp(self, cs: ConstraintStore):
         cv = cs.view()

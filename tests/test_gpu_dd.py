@@ -186,3 +186,56 @@ def test_dd_nccl_world1(orc, R):
     rep2 = dv.solve_lcp(cs)
     assert rep2["iterations"] == rep["iterations"]
     assert torch.equal(lam1, cs.lam[:len(ia)])
+
+
+# ------------------------------------------------------------ domain-decomposed ReLCP step
+
+def _dd_step_vs_oracle(orc, R, sc, K, max_recursions, rank=-1, uid=None):
+    """relcp_dd_step (LCP solves split over K parts) against the oracle's
+    Algorithm-1 step: same recursions and N_C per recursion, identical
+    (ia, ib, gen) rows, configurations to 1e-9 (both sides solve every LCP to
+    r <= 1e-12, as tests/test_gpu_parity.py _compare_step)."""
+    r = orc.relcp_step(sc, lcp_tol=1e-12, max_recursions=max_recursions)
+    dd = R.DomainDecomposition(_offsets(sc["n"], K), rank=rank, nccl_uid=uid, dynamics=sc["dynamics"],
+                               dt=sc["dt"], box=list(sc["box"]), cutoff=sc["cutoff"], eps_ncp=sc["eps_ncp"],
+                               xi=sc.get("xi", 1.0), lcp_tol=1e-12, lcp_max_iter=2_000_000,
+                               max_recursions=max_recursions)
+    bodies = R.BodyState.from_scene(sc)
+    cs = R.ConstraintStore(8 * max(1, len(r["constraints"]["ia"])) + 64)
+    rep = dd.step(bodies, cs)
+    assert rep["recursions"] == r["recursions"] and rep["n_c"] == r["n_c"]
+    assert (rep["status"] != 0) == (r["status"] != 0)
+    g, c = cs.to_numpy(), r["constraints"]
+    og, oo = np.lexsort((g["ib"], g["ia"], g["gen"])), np.lexsort((c["ib"], c["ia"], c["gen"]))
+    for k in ("ia", "ib", "gen"):
+        assert np.array_equal(g[k][og], c[k][oo])
+    dpos = bodies.pos.cpu().numpy() - r["pos"]
+    if np.all(sc["box"] > 0):
+        dpos -= sc["box"] * np.rint(dpos / sc["box"])
+    assert np.max(np.abs(dpos)) <= 1e-9
+    assert np.max(np.abs(bodies.quat.cpu().numpy() - r["quat"])) <= 1e-9
+    assert rep["max_overlap"] <= sc["eps_ncp"] or rep["status"] != 0
+    dd.close()
+    return rep, bodies, cs
+
+
+@pytest.mark.parametrize("K", [1, 2, 3])
+def test_dd_step_cfg5_recipe(orc, R, K):
+    """The bench workload's recipe at 1000 bodies, two augmentations."""
+    rep, _, _ = _dd_step_vs_oracle(orc, R, scenes.cfg5(n=1000), K, max_recursions=2)
+    assert rep["recursions"] == 2
+
+
+@pytest.mark.parametrize("K", [2, 4])
+def test_dd_step_cfg1(orc, R, K):
+    _dd_step_vs_oracle(orc, R, scenes.cfg1(), K, max_recursions=50)
+
+
+def test_dd_step_nccl_world1(orc, R):
+    """NCCL transport at world size 1: the same step as one virtual part, bitwise."""
+    sc = scenes.cfg5(n=1000)
+    rep_n, b_n, cs_n = _dd_step_vs_oracle(orc, R, sc, 1, 2, rank=0, uid=R.dd_nccl_unique_id())
+    rep_v, b_v, cs_v = _dd_step_vs_oracle(orc, R, sc, 1, 2)
+    assert rep_n["iterations"] == rep_v["iterations"]
+    assert torch.equal(b_n.pos, b_v.pos) and torch.equal(b_n.quat, b_v.quat) and torch.equal(b_n.vel, b_v.vel)
+    assert torch.equal(cs_n.lam[:cs_n.count], cs_v.lam[:cs_v.count])

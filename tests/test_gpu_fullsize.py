@@ -227,6 +227,17 @@ def test_fullsize_cfg3_step_planar(R):
     assert float(cs.n[2, :m][g0].abs().max()) < 1e-11
     assert float(cs.ta[0, :m][g0].abs().max()) < 1e-11 and float(cs.ta[1, :m][g0].abs().max()) < 1e-11
     assert bool(torch.all(cs.lam[:m] >= 0))
+    # the regime R21 describes, recorded: the first-order overdamped update turns
+    # jammed bodies by ~1 rad (measured 0.97 rad; dt |omega| is larger, the
+    # normalised first-order quaternion update saturates) in one dt = 1e-2 step:
+    # the recipe is stiff at this dt, which is why later generations may leave
+    # the plane
+    q0 = torch.as_tensor(sc["quat"], device="cuda")
+    q1 = bodies.quat / bodies.quat.norm(dim=1, keepdim=True)
+    q0 = q0 / q0.norm(dim=1, keepdim=True)
+    ang = 2.0 * torch.acos(torch.clamp((q0 * q1).sum(1).abs(), max=1.0))
+    print(f"cfg3 step: max rotation {float(ang.max()):.2f} rad, bodies turned > 1 rad: {int((ang > 1.0).sum())}")
+    assert float(ang.max()) > 0.5
 
 
 def test_fullsize_cfg5_A0_subbox_every_pair(orc, R, cfg5_full):
