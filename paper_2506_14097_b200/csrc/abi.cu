@@ -410,6 +410,7 @@ void relcp_default_params(relcp_params *p) {
     p->layout = RELCP_LAYOUT_AUTO;
     p->cluster = 1;
     p->snsd_cert = 1;
+    p->k6_pipe = 0;
 }
 
 int relcp_create(relcp_ctx **out, const relcp_params *p, void *cuda_stream) {

@@ -150,6 +150,7 @@ struct relcp_ctx {
     int64_t jds_solves = 0;  // solves on the JDS layout since the stats reset
     int64_t cluster_solves = 0;  // BB solves by the single-cluster loop since the reset
     int cl_ok = -1;          // cluster launch possible (-1: not probed yet)
+    int k6p_attr = 0;        // k_scatter_pipe's dynamic shared-memory limit set
     double L_reuse = 0.0;    // relcp_step: ||A|| of this step's previous LCP (0: none; R1)
     int64_t L_reuse_nc = 0;  // its row count
     DevBuf<long long> dstat; // (4) device-side counters: [0] SNSD multistart pairs

@@ -29,6 +29,7 @@
 #include "reduce.cuh"
 #include "rows.cuh"
 #include "k6k7.cuh"
+#include "k6pipe.cuh"
 
 #ifndef SCATTER_WPB
 #define SCATTER_WPB 4    // warps per block (same-box A/B: 4 x 8 blocks beats 8 x 4)
@@ -600,6 +601,36 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
         else if (mode == 2) k_scatter_jt<2><<<(unsigned)grid, 32 * JDS_WPB, 0, ctx->stream>>>(JDS_ARGS);
         else k_scatter_jt<0><<<(unsigned)grid, 32 * JDS_WPB, 0, ctx->stream>>>(JDS_ARGS);
 #undef JDS_ARGS
+        CKL();
+        return RELCP_OK;
+    }
+#ifndef K6_PIPE
+#define K6_PIPE 1
+#endif
+#ifndef K6_PIPE_MIN_BODIES
+#define K6_PIPE_MIN_BODIES 65536
+#endif
+    if (K6_PIPE && ctx->op_sorted && mode >= 0 && mode <= 2 && nb >= K6_PIPE_MIN_BODIES && ctx->p.k6_pipe) {
+        // TMA-staged K6 (k6pipe.cuh): persistent CTAs, K6P_MINB per SM
+        if (!ctx->k6p_attr) {
+            CK(cudaFuncSetAttribute(k_scatter_pipe<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, k6p::SMEM));
+            CK(cudaFuncSetAttribute(k_scatter_pipe<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, k6p::SMEM));
+            CK(cudaFuncSetAttribute(k_scatter_pipe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, k6p::SMEM));
+            ctx->k6p_attr = 1;
+        }
+        const int64_t nwarp = (nb + 31) / 32;
+        int64_t grid = (int64_t)RELCP_SM_COUNT * K6P_MINB;
+        if (grid > nwarp) grid = nwarp;
+        const K6Op o = op_k6(ctx);
+        if (mode == 1)
+            k_scatter_pipe<1><<<(unsigned)grid, K6P_NT, k6p::SMEM, ctx->stream>>>(o, x, g, xb, gb, ctx->st.p,
+                                                                                xscale_dev, U, F);
+        else if (mode == 2)
+            k_scatter_pipe<2><<<(unsigned)grid, K6P_NT, k6p::SMEM, ctx->stream>>>(o, x, g, xb, gb, ctx->st.p,
+                                                                                xscale_dev, U, F);
+        else
+            k_scatter_pipe<0><<<(unsigned)grid, K6P_NT, k6p::SMEM, ctx->stream>>>(o, x, g, xb, gb, ctx->st.p,
+                                                                                xscale_dev, U, F);
         CKL();
         return RELCP_OK;
     }

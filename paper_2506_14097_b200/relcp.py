@@ -39,7 +39,8 @@ class Params(ctypes.Structure):
     _fields_ = [("dynamics", i32), ("max_recursions", i32), ("dt", f64), ("eps_ncp", f64), ("cutoff", f64),
                 ("lcp_tol", f64), ("lcp_max_iter", i64), ("check_every", i32), ("power_iters", i32),
                 ("box", f64 * 3), ("xi", f64), ("n_dirs", i32), ("solver", i32), ("reorder", i32),
-                ("layout", i32), ("cluster", i32), ("snsd_cert", i32)]
+                ("layout", i32), ("cluster", i32), ("snsd_cert", i32),
+                ("k6_pipe", i32)]
 
 
 SOLVER_BB, SOLVER_APGD, SOLVER_APGD_FUSED = 0, 1, 2

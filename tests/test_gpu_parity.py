@@ -711,3 +711,52 @@ def test_cfg3_step_parity(orc, R):
     # planar symmetry: normals and torque arms stay in / normal to z = 0
     assert np.max(np.abs(g["n"][:, 2])) < 1e-11
     assert np.max(np.abs(r["pos"][:, 2])) < 1e-11
+
+
+@pytest.mark.parametrize("hubs", [False, True])
+@pytest.mark.parametrize("dynamics", [0, 1])
+def test_k6_pipe_bitwise(orc, R, hubs, dynamics):
+    """The TMA-staged K6 (params.k6_pipe, from 65,536 bodies)
+    computes exactly the per-warp kernel's sums: apply, wrench and a fixed
+    number of BB iterations are bitwise equal with the pipeline on and off,
+    and the apply matches the oracle at 1e-12.  hubs: bodies with 300-700
+    rows make some 32-body groups larger than a stage (warp-0 fallback)."""
+    nb, nc = 70_000, 200_000
+    b, ia, ib, n, ra, rb = scenes.local_constraint_network(nb, nc, 31, dynamics)
+    if hubs:
+        rng = np.random.default_rng(3)
+        hi = np.concatenate([np.full(700, 1000), np.full(300, 40000)])
+        hj = np.concatenate([rng.integers(1001, nb, 700), rng.integers(40001, nb, 300)])
+        ia, ib = np.concatenate([ia, hi]).astype(np.int32), np.concatenate([ib, hj]).astype(np.int32)
+        n = np.concatenate([n, rng.normal(size=(1000, 3))])
+        n /= np.linalg.norm(n, axis=1, keepdims=True)
+        ra = np.concatenate([ra, rng.uniform(-0.7, 0.7, (1000, 3))])
+        rb = np.concatenate([rb, rng.uniform(-0.7, 0.7, (1000, 3))])
+        o = np.lexsort((ib, ia))
+        ia, ib, n, ra, rb = ia[o], ib[o], n[o], ra[o], rb[o]
+    ta, tb = np.cross(ra, n), np.cross(rb, n)
+    m = len(ia)
+    x = np.random.default_rng(4).standard_normal(m)
+    W = orc.body_W(b)
+    y_ref = orc.delassus_apply(W, ia, ib, n, ta, tb, 1e-6, x)
+    bodies = R.BodyState.from_scene(b)
+    xd = torch.as_tensor(x, device="cuda")
+    q = torch.as_tensor(np.random.default_rng(5).standard_normal(m) * 1e-6, device="cuda")
+    out = []
+    for pipe in (0, 1):
+        ctx = _ctx(R, dict(dynamics=dynamics, dt=1e-3, cutoff=0.1, eps_ncp=1e-5, box=[0, 0, 0]), k6_pipe=pipe,
+                   lcp_tol=1e-30, lcp_max_iter=40, layout=0)
+        cs = R.ConstraintStore.from_rows(ia, ib, n, ta, tb)
+        ctx.prepare_operator(bodies, cs)
+        y = torch.empty_like(xd)
+        ctx.delassus_apply(bodies, cs, xd, y, 1e-6)
+        assert np.max(np.abs(y.cpu().numpy() - y_ref)) <= 1e-12 * np.max(np.abs(y_ref))
+        F = torch.empty(nb, 6, dtype=torch.float64, device="cuda")
+        U = torch.empty_like(F)
+        ctx.wrench(bodies, cs, xd, F, U)
+        cs.q[:m] = q
+        rep = ctx.solve_lcp(bodies, cs)
+        out.append((y, F, U, cs.lam[:m].clone(), cs.g[:m].clone(), rep["iterations"]))
+    for a, c in zip(out[0][:5], out[1][:5]):
+        assert torch.equal(a, c)
+    assert out[0][5] == out[1][5] == 40
