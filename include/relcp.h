@@ -105,10 +105,9 @@ typedef struct relcp_params {
                              of curvature of A + B (curvature certificate,
                              DESIGN.md R29) [1]; 0 = always multistart.      */
     int32_t k6_pipe;      /* 1: K6 of sorted CSR stores from 65,536 bodies runs
-                             the TMA-staged pipeline (k6pipe.cuh; bitwise equal
-                             to the per-warp kernel, measured 3.6x slower:
-                             ~26 small bulk copies per 32-body group, DESIGN.md
-                             §5) [0]                                          */
+                             the TMA-staged pipeline over per-group records
+                             (k6pipe.cuh; bitwise equal to the per-warp kernel,
+                             measured 3.1x slower) [0]          */
 } relcp_params;
 
 #define RELCP_REORDER_OFF 0

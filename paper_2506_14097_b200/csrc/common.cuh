@@ -151,6 +151,9 @@ struct relcp_ctx {
     int64_t cluster_solves = 0;  // BB solves by the single-cluster loop since the reset
     int cl_ok = -1;          // cluster launch possible (-1: not probed yet)
     int k6p_attr = 0;        // k_scatter_pipe's dynamic shared-memory limit set
+    int op_k6r = 0;          // per-group K6 records built (k6pipe.cuh)
+    DevBuf<long long> k6r_sz, k6r_off;  // (groups + 1) record sizes / offsets (bytes)
+    DevBuf<unsigned char> k6r_rec;      // the records
     double L_reuse = 0.0;    // relcp_step: ||A|| of this step's previous LCP (0: none; R1)
     int64_t L_reuse_nc = 0;  // its row count
     DevBuf<long long> dstat; // (4) device-side counters: [0] SNSD multistart pairs

@@ -30,6 +30,12 @@
 #include "rows.cuh"
 #include "k6k7.cuh"
 #include "k6pipe.cuh"
+#ifndef K6_PIPE
+#define K6_PIPE 1
+#endif
+#ifndef K6_PIPE_MIN_BODIES
+#define K6_PIPE_MIN_BODIES 65536
+#endif
 
 #ifndef SCATTER_WPB
 #define SCATTER_WPB 4    // warps per block (same-box A/B: 4 x 8 blocks beats 8 x 4)
@@ -341,6 +347,24 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
                                                               ctx->ew.p);
         CKL();
     }
+    // per-group records of the TMA-staged K6 (k6pipe.cuh; params.k6_pipe)
+    ctx->op_k6r = 0;
+    if (K6_PIPE && nc > 0 && !jds && sorted && ctx->p.k6_pipe && nb >= K6_PIPE_MIN_BODIES) {
+        const int64_t nw = (nb + 31) / 32;
+        CK(ctx->k6r_sz.grow(nw + 1));
+        CK(ctx->k6r_off.grow(nw + 1));
+        CK(cudaMemsetAsync(ctx->k6r_sz.p + nw, 0, sizeof(long long), ctx->stream));
+        k_k6r_size<<<grid_for(nw), RELCP_NT, 0, ctx->stream>>>(nb, ctx->pa.p, ctx->row_ptr.p, ctx->k6r_sz.p);
+        CKL();
+        long long tot = 0;
+        CKS(scan_exclusive_ll(ctx, ctx->k6r_sz.p, ctx->k6r_off.p, nw + 1, &tot));
+        CK(ctx->k6r_rec.grow((size_t)tot + 16));
+        k_k6r_fill<<<grid_for(32 * nw, 256, 8), 256, 0, ctx->stream>>>(nb, ctx->pa.p, ctx->row_ptr.p, ctx->k6r_off.p,
+                                                                       cs->n, cs->ta, cs->capacity, ctx->ecid.p,
+                                                                       ctx->ew.p, nc, ctx->W.p, ctx->k6r_rec.p);
+        CKL();
+        ctx->op_k6r = 1;
+    }
     ctx->op_sorted = sorted;
     ctx->op_cap = cs->capacity;
     ctx->op_rs = nc;
@@ -604,13 +628,7 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
         CKL();
         return RELCP_OK;
     }
-#ifndef K6_PIPE
-#define K6_PIPE 1
-#endif
-#ifndef K6_PIPE_MIN_BODIES
-#define K6_PIPE_MIN_BODIES 65536
-#endif
-    if (K6_PIPE && ctx->op_sorted && mode >= 0 && mode <= 2 && nb >= K6_PIPE_MIN_BODIES && ctx->p.k6_pipe) {
+    if (K6_PIPE && ctx->op_k6r && mode >= 0 && mode <= 2) {
         // TMA-staged K6 (k6pipe.cuh): persistent CTAs, K6P_MINB per SM
         if (!ctx->k6p_attr) {
             CK(cudaFuncSetAttribute(k_scatter_pipe<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, k6p::SMEM));
@@ -623,14 +641,14 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
         if (grid > nwarp) grid = nwarp;
         const K6Op o = op_k6(ctx);
         if (mode == 1)
-            k_scatter_pipe<1><<<(unsigned)grid, K6P_NT, k6p::SMEM, ctx->stream>>>(o, x, g, xb, gb, ctx->st.p,
-                                                                                xscale_dev, U, F);
+            k_scatter_pipe<1><<<(unsigned)grid, K6P_NT, k6p::SMEM, ctx->stream>>>(
+                o, ctx->k6r_rec.p, ctx->k6r_off.p, x, g, xb, gb, ctx->st.p, xscale_dev, U, F);
         else if (mode == 2)
-            k_scatter_pipe<2><<<(unsigned)grid, K6P_NT, k6p::SMEM, ctx->stream>>>(o, x, g, xb, gb, ctx->st.p,
-                                                                                xscale_dev, U, F);
+            k_scatter_pipe<2><<<(unsigned)grid, K6P_NT, k6p::SMEM, ctx->stream>>>(
+                o, ctx->k6r_rec.p, ctx->k6r_off.p, x, g, xb, gb, ctx->st.p, xscale_dev, U, F);
         else
-            k_scatter_pipe<0><<<(unsigned)grid, K6P_NT, k6p::SMEM, ctx->stream>>>(o, x, g, xb, gb, ctx->st.p,
-                                                                                xscale_dev, U, F);
+            k_scatter_pipe<0><<<(unsigned)grid, K6P_NT, k6p::SMEM, ctx->stream>>>(
+                o, ctx->k6r_rec.p, ctx->k6r_off.p, x, g, xb, gb, ctx->st.p, xscale_dev, U, F);
         CKL();
         return RELCP_OK;
     }
