@@ -6,6 +6,7 @@
 #include <stdio.h>
 #include <stdarg.h>
 #include <string.h>
+#include <utility>
 
 #include "../../include/relcp.h"
 
@@ -150,6 +151,7 @@ struct relcp_ctx {
     int64_t jds_solves = 0;  // solves on the JDS layout since the stats reset
     int64_t cluster_solves = 0;  // BB solves by the single-cluster loop since the reset
     int cl_ok = -1;          // cluster launch possible (-1: not probed yet)
+    int pdl = 0;             // K6 / K7 launches with programmatic dependent launch (lcp.cu batches)
     int k6p_attr = 0;        // k_scatter_pipe's dynamic shared-memory limit set
     int op_k6r = 0;          // per-group K6 records built (k6pipe.cuh)
     DevBuf<long long> k6r_sz, k6r_off;  // (groups + 1) record sizes / offsets (bytes)
@@ -250,6 +252,32 @@ static inline int grid_for(int64_t n, int nt = RELCP_NT, int per_sm = 8) {
     if (g > cap) g = cap;
     if (g < 1) g = 1;
     return (int)g;
+}
+
+// ------------------------------------------------------------ programmatic dependent launch
+// The LCP iteration kernels (K6, K7) are launched with programmatic stream
+// serialisation when ctx->pdl is set (inside the solve's batches): the next
+// kernel's CTAs are scheduled while the previous one drains, and wait in
+// pdl_wait() (griddepcontrol.wait: the previous grid completed and its memory
+// is visible) before touching its outputs; pdl_open() lets the next kernel be
+// scheduled early.  Both are no-ops for a plain launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_open() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_k(bool pdl, void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, cudaStream_t st,
+                                   Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
 }
 
 // ------------------------------------------------------------ internal API

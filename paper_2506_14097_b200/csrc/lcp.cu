@@ -182,6 +182,8 @@ __global__ void __launch_bounds__(RELCP_NT, CR ? ITER_MINB_CR : ITER_MINB) k_lcp
                                                        double *xB, double *gB, double *part, unsigned *counter,
                                                        LcpState *st, double *acc_out) {
     __shared__ double sh[6 * 32];
+    pdl_wait();
+    pdl_open();
     if (st->done) return;
     const double alpha = st->alpha;
     const bool fix = st->fix != 0;
@@ -255,6 +257,8 @@ __global__ void __launch_bounds__(RELCP_NT, CR ? ITER_MINB_CR : ITER_MINB) k_apg
     const double *__restrict__ rc, const double *__restrict__ U, double s, const double *__restrict__ q, double *xA, double *gA, double *xB,
     double *gB, double *part, unsigned *counter, LcpState *st) {
     __shared__ double sh[3 * 32];
+    pdl_wait();
+    pdl_open();
     if (st->done) return;
     const double t = st->alpha, beta = st->beta;
     double *xc = xA, *gc = gA, *xp = xB, *gp = gB;
@@ -652,7 +656,15 @@ static int lcp_solve_view(relcp_ctx *ctx, const relcp_bodies *b, relcp_constrain
         }
     } graph_guard{gexec};
     // `batch` BB iterations: K6 (scatter + projection) then K7 (gather + update)
+#ifndef RELCP_PDL
+#define RELCP_PDL 1
+#endif
     auto enqueue_batch = [&]() -> int {
+        ctx->pdl = RELCP_PDL;  // K6 / K7 of the batch: programmatic dependent launches
+        struct PdlOff {
+            relcp_ctx *c;
+            ~PdlOff() { c->pdl = 0; }
+        } pdl_off{ctx};
         for (int j = 0; j < batch; ++j) {
             // per-kernel events only for direct (uncaptured) batches in timing mode
             const bool ev_on = ctx->timing && !capturing;
@@ -669,17 +681,17 @@ static int lcp_solve_view(relcp_ctx *ctx, const relcp_bodies *b, relcp_constrain
             CKS(op_scatter(ctx, nb, cs->lambda, cs->g, apgd ? 2 : 1, nullptr, ctx->U.p, nullptr, xB, gB, sl));
             if (ev_on) CK(cudaEventRecord(ctx->ev[3 * j + 1], st));
             if (apgd && cr)
-                k_apgd_iter<true><<<gridi, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g, xB,
-                                                              gB, ctx->partials.p, ctx->counter.p, ctx->st.p);
+                CK(launch_k(ctx->pdl, k_apgd_iter<true>, gridi, RELCP_NT, 0, st, ROWS_ARGS, ctx->U.p, s, cs->q,
+                            cs->lambda, cs->g, xB, gB, ctx->partials.p, ctx->counter.p, ctx->st.p));
             else if (apgd)
-                k_apgd_iter<false><<<gridi, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g, xB,
-                                                               gB, ctx->partials.p, ctx->counter.p, ctx->st.p);
+                CK(launch_k(ctx->pdl, k_apgd_iter<false>, gridi, RELCP_NT, 0, st, ROWS_ARGS, ctx->U.p, s, cs->q,
+                            cs->lambda, cs->g, xB, gB, ctx->partials.p, ctx->counter.p, ctx->st.p));
             else if (cr)
-                k_lcp_iter<true><<<gridi, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g, xB,
-                                                             gB, ctx->partials.p, ctx->counter.p, ctx->st.p, nullptr);
+                CK(launch_k(ctx->pdl, k_lcp_iter<true>, gridi, RELCP_NT, 0, st, ROWS_ARGS, ctx->U.p, s, cs->q,
+                            cs->lambda, cs->g, xB, gB, ctx->partials.p, ctx->counter.p, ctx->st.p, (double *)nullptr));
             else
-                k_lcp_iter<false><<<gridi, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g, xB,
-                                                              gB, ctx->partials.p, ctx->counter.p, ctx->st.p, nullptr);
+                CK(launch_k(ctx->pdl, k_lcp_iter<false>, gridi, RELCP_NT, 0, st, ROWS_ARGS, ctx->U.p, s, cs->q,
+                            cs->lambda, cs->g, xB, gB, ctx->partials.p, ctx->counter.p, ctx->st.p, (double *)nullptr));
             CKL();
             if (ev_on) CK(cudaEventRecord(ctx->ev[3 * j + 2], st));
         }

@@ -399,6 +399,8 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
     // contributions staged as 3 planes of double2 (components 01, 23, 45):
     // 128-bit shared loads in the per-lane segment sums
     __shared__ double2 sm[SCATTER_WPB][3][SCATTER_TILE + 1];
+    pdl_wait();
+    pdl_open();
     if (MODE != 0 && st->done) return;
     const XEff xe = xeff_setup<MODE>(st, x, g, xb, gb, xscale);
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -440,6 +442,8 @@ __global__ void __launch_bounds__(32 * JDS_WPB, JT_MINB) k_scatter_jt(
     double *__restrict__ U, double *__restrict__ Fout) {
     __shared__ double2 sm[JDS_WPB][3][JT_TILE];
     __shared__ double sa_[JDS_WPB][6][32];
+    pdl_wait();
+    pdl_open();
     double alpha = 0.0, beta = 0.0, tl = 1.0;
     bool fix = false;
     const double *xc = x, *gc = g, *xp = xb, *gp = gb;
@@ -621,8 +625,8 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
 #define JDS_ARGS nb, nc, ctx->pa.p, ctx->row_ptr.p, ctx->jameta.p, ctx->jbmeta.p, ctx->rc.p, ctx->jbcid.p, \
                  ctx->jbpay.p, x, g, xb, gb, ctx->st.p, xscale_dev, ctx->W.p, U, F
         if (mode < 0 || mode > 2) return set_err(ctx, RELCP_E_STATE, "JDS scatter: mode %d unsupported", mode);
-        if (mode == 1) k_scatter_jt<1><<<(unsigned)grid, 32 * JDS_WPB, 0, ctx->stream>>>(JDS_ARGS);
-        else if (mode == 2) k_scatter_jt<2><<<(unsigned)grid, 32 * JDS_WPB, 0, ctx->stream>>>(JDS_ARGS);
+        if (mode == 1) CK(launch_k(ctx->pdl, k_scatter_jt<1>, (unsigned)grid, 32 * JDS_WPB, 0, ctx->stream, JDS_ARGS));
+        else if (mode == 2) CK(launch_k(ctx->pdl, k_scatter_jt<2>, (unsigned)grid, 32 * JDS_WPB, 0, ctx->stream, JDS_ARGS));
         else k_scatter_jt<0><<<(unsigned)grid, 32 * JDS_WPB, 0, ctx->stream>>>(JDS_ARGS);
 #undef JDS_ARGS
         CKL();
@@ -668,8 +672,8 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
         if (!ctx->op_sorted) return set_err(ctx, RELCP_E_STATE, "fused solver needs a store sorted by ia");
         k_scatter<3, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
     } else if (ctx->op_sorted) {
-        if (mode == 1) k_scatter<1, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
-        else if (mode == 2) k_scatter<2, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+        if (mode == 1) CK(launch_k(ctx->pdl, k_scatter<1, true>, G, T, 0, ctx->stream, SCATTER_ARGS));
+        else if (mode == 2) CK(launch_k(ctx->pdl, k_scatter<2, true>, G, T, 0, ctx->stream, SCATTER_ARGS));
         else k_scatter<0, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
     } else {
         if (mode == 1) k_scatter<1, false><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
