@@ -16,6 +16,9 @@
 struct V6 {
     double v[6];
 };
+// double2 per warp for k6_group's staging: 3 planes of SCATTER_TILE + 1 entries,
+// and at least 192 (the U / F transpose: 2 x 192 doubles)
+#define K6_SMEM_D2 (3 * (SCATTER_TILE + 1) > 192 ? 3 * (SCATTER_TILE + 1) : 192)
 
 // CSR operator of a prepared context (op_prepare)
 struct K6Op {

@@ -379,7 +379,7 @@ namespace cg = cooperative_groups;
 template <bool SORTED, bool CR>
 __global__ void __launch_bounds__(CL_NT, 1) k_bb_cluster(int iters, K6Op o, K7Rows r, double *xA, double *gA,
                                                          double *xB, double *gB, double *U, LcpState *gst) {
-    extern __shared__ double2 cl_dyn[];  // CL_WARPS x 3 x (SCATTER_TILE + 1): K6 staging
+    extern __shared__ double2 cl_dyn[];  // CL_WARPS x K6_SMEM_D2: K6 staging
     __shared__ LcpState st;
     __shared__ double part[6];
     __shared__ double sh[6 * 32];
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(CL_NT, 1) k_bb_cluster(int iters, K6Op o, K7Ro
     if (threadIdx.x == 0) st = *gst;
     __syncthreads();
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-    auto c6 = reinterpret_cast<double2(*)[SCATTER_TILE + 1]>(cl_dyn + wl * 3 * (SCATTER_TILE + 1));
+    auto c6 = reinterpret_cast<double2(*)[SCATTER_TILE + 1]>(cl_dyn + wl * K6_SMEM_D2);
     const int64_t nwarp = (o.nb + 31) >> 5;
     const int ops[6] = {0, 0, 0, 1, 1, 0};
     for (int it = 0; it < iters && !st.done; ++it) {
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(CL_NT, 1) k_bb_cluster(int iters, K6Op o, K7Ro
 static int cluster_probe(relcp_ctx *ctx) {
     if (ctx->cl_ok >= 0) return ctx->cl_ok;
     ctx->cl_ok = 0;
-    const size_t dyn = sizeof(double2) * CL_WARPS * 3 * (SCATTER_TILE + 1);
+    const size_t dyn = sizeof(double2) * CL_WARPS * K6_SMEM_D2;
     void (*ks[4])(int, K6Op, K7Rows, double *, double *, double *, double *, double *, LcpState *) = {
         k_bb_cluster<true, true>, k_bb_cluster<true, false>, k_bb_cluster<false, true>, k_bb_cluster<false, false>};
     for (auto k : ks) {
@@ -476,7 +476,7 @@ static int cluster_launch(relcp_ctx *ctx, int iters, bool sorted, bool cr, const
     at[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(CL_CTAS);
     cfg.blockDim = dim3(CL_NT);
-    cfg.dynamicSmemBytes = sizeof(double2) * CL_WARPS * 3 * (SCATTER_TILE + 1);
+    cfg.dynamicSmemBytes = sizeof(double2) * CL_WARPS * K6_SMEM_D2;
     cfg.stream = ctx->stream;
     cfg.attrs = at;
     cfg.numAttrs = 1;

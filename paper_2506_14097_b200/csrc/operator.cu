@@ -386,7 +386,7 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
 // b-side entries (+[n; t_b]).  Otherwise row_ptr / ecid / ew hold both sides.
 // Per-body order: a-side rows, then CSR entries -- fixed, deterministic.
 // the U / F transpose reuses a warp's staging area: 2 x 32 x 6 doubles
-static_assert(3 * (SCATTER_TILE + 1) * 2 >= 2 * 192, "SCATTER_TILE too small for the U/F staging");
+
 
 // MODE: 0 apply (x_eff = x), 1 BB step (x_eff = max(0, x - alpha g)),
 // 2 APGD step (y = x + beta (x - x'), g_y likewise, x_eff = max(0, y - t g_y);
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
     double *__restrict__ U, double *__restrict__ Fout, const double *__restrict__ Fa) {
     // contributions staged as 3 planes of double2 (components 01, 23, 45):
     // 128-bit shared loads in the per-lane segment sums
-    __shared__ double2 sm[SCATTER_WPB][3][SCATTER_TILE + 1];
+    __shared__ double2 sm[SCATTER_WPB][K6_SMEM_D2];
     pdl_wait();
     pdl_open();
     if (MODE != 0 && st->done) return;
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
         // K7 (ascending) touched last (still in L2) and ends on the bodies whose
         // U / rows K7 touches first
         const int64_t w = K6_REVERSE ? nwarp - 1 - wi : wi;
-        k6_group<MODE, SORTED>(w, o, xe, sm[wl], lane, U, Fout, Fa);
+        k6_group<MODE, SORTED>(w, o, xe, reinterpret_cast<double2(*)[SCATTER_TILE + 1]>(sm[wl]), lane, U, Fout, Fa);
     }
 }
 
