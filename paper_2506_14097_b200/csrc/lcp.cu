@@ -25,10 +25,11 @@
 #define ITER_MINB 4  // resident K7 blocks per SM (register budget); grid = 148 * ITER_MINB
 #endif
 #ifndef ITER_MINB_CR
-#define ITER_MINB_CR 2  // with compact rows (decode registers, 128 per thread): same-box A/B
-#endif                  // ILP 4 x 2 blocks 0.273 ms per iteration, ILP 2 x 3 blocks 0.276, ILP 1 x 4 0.283
+#define ITER_MINB_CR 2  // with compact rows (decode registers, 128 per thread): same-box A/B, round 2
+#endif                  // (K7 on the relaxed cfg5 store / cfg3 iteration): ILP 3 x 2 blocks 153 us / 31.0 us,
+                        // ILP 4 x 2 165 / 32.4, ILP 2 x 3 168 / 34.9, ILP 1 x 4 163 / 37.5, ILP 5-6 x 2 181-195
 #ifndef ITER_ILP_CR
-#define ITER_ILP_CR 4
+#define ITER_ILP_CR 3
 #endif
 #ifndef ITER_ILP
 #define ITER_ILP 2   // rows per thread per trip in K7
