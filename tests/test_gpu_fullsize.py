@@ -333,6 +333,46 @@ def test_fullsize_cfg5_relaxed_complete_step(orc, R, cfg5_full):
     assert float(np.max(np.abs(np.minimum(c["lam"], c["g"])))) <= 1e-8
 
 
+def test_fullsize_cfg5_relaxed_dd_step(orc, R, cfg5_full):
+    """The headline step, domain-decomposed (relcp_dd_step, 4 virtual parts of
+    500k bodies): the same complete Algorithm-1 step as the
+    single-domain library -- same recursions, N_C per recursion and rows
+    (ia, ib, gen bit-exact), every LCP to r <= 1e-8, status 0 -- with
+    configurations equal to the solver tolerance's effect, and g = the
+    oracle's s D^T W D lambda + q on every row."""
+    from paper_2506_14097_b200 import drivers
+    lit = cfg5_full
+    pos, quat, _ = drivers.relax(lit, max_recursions=0, lcp_max_iter=20000, max_steps=60)
+    sc = scenes.with_state(lit, pos.cpu().numpy(), quat.cpu().numpy(), 55, "cfg5-relaxed")
+    kw = dict(lcp_tol=1e-8, lcp_max_iter=200_000, max_recursions=50)
+    ctx = _ctx(R, sc, **kw)
+    b1 = R.BodyState.from_scene(sc)
+    c1 = R.ConstraintStore(12 * sc["n"])
+    r1 = ctx.step(b1, c1)
+    dd = R.DomainDecomposition(np.array([0, 500_000, 1_000_000, 1_500_000, 2_000_000], dtype=np.int64),
+                               dynamics=sc["dynamics"], dt=sc["dt"], box=list(sc["box"]), cutoff=sc["cutoff"],
+                               eps_ncp=sc["eps_ncp"], **kw)
+    b2 = R.BodyState.from_scene(sc)
+    c2 = R.ConstraintStore(12 * sc["n"])
+    r2 = dd.step(b2, c2)
+    assert r2["rc"] == 0 and r2["status"] == 0 and max(r2["residuals"]) <= 1e-8, r2
+    assert r2["recursions"] == r1["recursions"] and r2["n_c"] == r1["n_c"]
+    assert r2["max_overlap"] <= sc["eps_ncp"]
+    g1, g2 = c1.to_numpy(), c2.to_numpy()
+    for k in ("ia", "ib", "gen"):
+        assert np.array_equal(g1[k], g2[k]), k
+    dpos = b2.pos.cpu().numpy() - b1.pos.cpu().numpy()
+    dpos -= sc["box"] * np.rint(dpos / sc["box"])
+    print(f"dd step: recursions {r2['recursions']}, iterations {r2['iterations']} vs {r1['iterations']}, "
+          f"max |dpos| {np.max(np.abs(dpos)):.2e}")
+    assert np.max(np.abs(dpos)) <= 1e-6
+    Alam = orc.delassus_apply(orc.body_W(sc), g2["ia"], g2["ib"], g2["n"], g2["ta"], g2["tb"], sc["dt"] ** 2,
+                              g2["lam"])
+    assert np.max(np.abs(g2["g"] - (Alam + g2["q"]))) <= 1e-12 * np.max(np.abs(Alam))
+    assert np.all(g2["lam"] >= 0) and float(np.max(np.abs(np.minimum(g2["lam"], g2["g"])))) <= 1e-8
+    dd.close()
+
+
 def _cfg4_fixture():
     import os
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "cfg4_full_sample.txt")
