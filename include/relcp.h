@@ -447,12 +447,15 @@ int relcp_dd_get_u(relcp_dd *dd, double *U);
 int relcp_dd_solve_lcp(relcp_dd *dd, relcp_constraints *cs, relcp_solve_report *rep);
 /* One ReLCP step (Algorithm 1; same contract, report and codes as
  * relcp_step, in the caller's body order) whose LCP solves are the
- * domain-decomposed BB solve above on each recursion's store; generation,
- * checks and augmentation are replicated on every rank (every rank passes
- * all bodies and the whole store; the single-domain kernels are
- * deterministic, so every rank holds the same store).  NCCL: after each solve
- * the ranks exchange their rows' lambda and g (grouped send / recv).
- * DESIGN.md §8. */
+ * domain-decomposed BB solve above on each recursion's store, and whose SNSD
+ * phases (generation at C^k, every check at the trial configuration) are
+ * split by the owner of i: each part scans the candidate pairs of its bodies.
+ * The broadphase, trial configuration, q and the store merge are replicated
+ * (every rank passes all bodies and the whole store and, after the exchanges,
+ * holds the same store, in the single-domain row order).  NCCL: after each
+ * SNSD phase the ranks all-reduce the counts and statistics and exchange their
+ * appended rows; after each solve their rows' lambda and g (grouped send /
+ * recv).  DESIGN.md §8. */
 int relcp_dd_step(relcp_dd *dd, relcp_bodies *bodies, const double *f_ext, relcp_constraints *cs,
                   relcp_step_report *rep);
 

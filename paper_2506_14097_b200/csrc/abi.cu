@@ -4,6 +4,8 @@
 
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX3: phase ranges for Nsight timelines
 
+#include <vector>
+
 #include "common.cuh"
 #include "reduce.cuh"
 
@@ -242,7 +244,7 @@ static int grow_pair_tmp(relcp_ctx *ctx, int64_t np) {
 // Returns the number of flagged pairs in *nflag, min phi, counts.
 static int snsd_flag_scan(relcp_ctx *ctx, const double *pos, const int32_t *shape, const double *axes,
                           double thresh, int *nflag, double *minphi, int64_t *ndegen, int64_t *nnonconv) {
-    const int64_t np = ctx->npairs;
+    const int64_t p0 = ctx->pair_lo, np = ctx->pair_n >= 0 ? ctx->pair_n : ctx->npairs;
     CKS(grow_pair_tmp(ctx, np));
     *nflag = 0;
     *minphi = INFINITY;
@@ -252,8 +254,8 @@ static int snsd_flag_scan(relcp_ctx *ctx, const double *pos, const int32_t *shap
     if (np >= (1ll << 31) - 1) return set_err(ctx, RELCP_E_ARG, "too many candidate pairs");
     // pairs whose lower bound Phi >= F(d/|d|) is >= max(thresh, 0) can neither be
     // flagged nor lower min(Phi) below 0: they are not solved (status 3)
-    CKS(geo_snsd(ctx, np, ctx->pi.p, ctx->pj.p, pos, ctx->Sig.p, ctx->tphi.p, ctx->tn.p, ctx->tra.p, ctx->trb.p,
-                 ctx->tstat.p, np, thresh > 0.0 ? thresh : 0.0, shape, axes));
+    CKS(geo_snsd(ctx, np, ctx->pi.p + p0, ctx->pj.p + p0, pos, ctx->Sig.p, ctx->tphi.p, ctx->tn.p, ctx->tra.p,
+                 ctx->trb.p, ctx->tstat.p, np, thresh > 0.0 ? thresh : 0.0, shape, axes));
     PHASE(ctx, "snsd.kernels");
     k_flag<<<grid_for(np), RELCP_NT, 0, ctx->stream>>>(np, ctx->tphi.p, ctx->tstat.p, thresh, ctx->tflag.p,
                                                        ctx->partials.p, ctx->counter.p, ctx->red.p);
@@ -274,10 +276,10 @@ static int snsd_flag_scan(relcp_ctx *ctx, const double *pos, const int32_t *shap
 }
 
 static int append_flagged(relcp_ctx *ctx, relcp_constraints *cs, int gen, int64_t nflag) {
-    const int64_t np = ctx->npairs;
+    const int64_t p0 = ctx->pair_lo, np = ctx->pair_n >= 0 ? ctx->pair_n : ctx->npairs;
     if (nflag == 0) return RELCP_OK;
     int *off = (int *)ctx->scan_ll.p;
-    k_append<<<grid_for(np), RELCP_NT, 0, ctx->stream>>>(np, ctx->tflag.p, off, ctx->pi.p, ctx->pj.p, ctx->tphi.p,
+    k_append<<<grid_for(np), RELCP_NT, 0, ctx->stream>>>(np, ctx->tflag.p, off, ctx->pi.p + p0, ctx->pj.p + p0, ctx->tphi.p,
                                                          ctx->tn.p, ctx->tra.p, ctx->trb.p, np, cs->count, gen,
                                                          cs->capacity, cs->ia, cs->ib, cs->gen, cs->n, cs->ta, cs->tb,
                                                          cs->phi, cs->q, cs->lambda);
@@ -290,8 +292,109 @@ static double op_s(const relcp_ctx *ctx) {
 }
 static double op_sigma(const relcp_ctx *ctx) { return ctx->p.dynamics == RELCP_INERTIAL ? ctx->p.dt : 1.0; }
 
+// first pair of every part: pairs are sorted by i, part k owns i in [off[k], off[k+1])
+__global__ void k_pair_bounds(int64_t np, const int *__restrict__ pi, int K, const int64_t *__restrict__ off,
+                              long long *__restrict__ out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k > K) return;
+    const int64_t key = off[k];
+    int64_t lo = 0, hi = np;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)pi[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    out[k] = lo;
+}
+
+// SNSD + flag (+ append when `append`) over the candidate pairs, whole or split
+// over the parts of `ds` (DistSpec); the appended rows of all parts land at
+// cs->count in part order (the single-domain order: pairs sorted by i), and
+// cs->count advances by the total.  Returns the statistics of all parts.
+static int flag_append(relcp_ctx *ctx, const double *pos, const int32_t *shape, const double *axes, double thresh,
+                       relcp_constraints *cs, int gen, bool append, const DistSpec *ds, int64_t *nflag_out,
+                       double *minphi_out, int64_t *ndeg_out, int64_t *nnc_out) {
+    if (!ds || ds->K <= 1) {
+        ctx->pair_lo = 0;
+        ctx->pair_n = -1;
+        int nflag;
+        CKS(snsd_flag_scan(ctx, pos, shape, axes, thresh, &nflag, minphi_out, ndeg_out, nnc_out));
+        *nflag_out = nflag;
+        if (append && nflag > 0 && *ndeg_out == 0 && cs->count + nflag <= cs->capacity) {
+            CKS(append_flagged(ctx, cs, gen, nflag));
+            cs->count += nflag;
+        }
+        return RELCP_OK;
+    }
+    const int K = ds->K;
+    std::vector<long long> pb(K + 1);
+    {
+        DevBuf<int64_t> doff;
+        DevBuf<long long> dpb;
+        CK(doff.grow(K + 1));
+        CK(dpb.grow(K + 1));
+        CK(cudaMemcpyAsync(doff.p, ds->off, sizeof(int64_t) * (K + 1), cudaMemcpyHostToDevice, ctx->stream));
+        k_pair_bounds<<<1, 64 * ((K + 64) / 64), 0, ctx->stream>>>(ctx->npairs, ctx->pi.p, K, doff.p, dpb.p);
+        CKL();
+        CK(cudaMemcpyAsync(pb.data(), dpb.p, sizeof(long long) * (K + 1), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    std::vector<double> vals(K + 4, 0.0);
+    vals[K + 3] = -INFINITY;  // -min Phi
+    const int64_t guard0 = ctx->n_guard_total;
+    std::vector<int64_t> cnt(K, 0);
+    const int64_t base = cs->count;
+    int64_t placed = 0;
+    for (int k = 0; k < K; ++k) {
+        if (ds->rank >= 0 && k != ds->rank) continue;
+        ctx->pair_lo = pb[k];
+        ctx->pair_n = pb[k + 1] - pb[k];
+        int nflag;
+        double mp;
+        int64_t nd, nn;
+        CKS(snsd_flag_scan(ctx, pos, shape, axes, thresh, &nflag, &mp, &nd, &nn));
+        cnt[k] = nflag;
+        vals[k] = nflag;
+        vals[K] += nd;
+        vals[K + 1] += nn;
+        vals[K + 3] = fmax(vals[K + 3], -mp);
+        // VIRTUAL: append each part at once, in part order (the next part's scan reuses the temporaries)
+        if (ds->rank < 0 && append && nflag > 0 && nd == 0 && base + placed + nflag <= cs->capacity) {
+            cs->count = base + placed;
+            CKS(append_flagged(ctx, cs, gen, nflag));
+        }
+        placed += nflag;
+    }
+    vals[K + 2] = (double)(ctx->n_guard_total - guard0);
+    ctx->n_guard_total = guard0;
+    if (ds->rank >= 0 && ds->reduce) CKS(ds->reduce(ds->user, vals.data(), K + 4));
+    int64_t total = 0;
+    for (int k = 0; k < K; ++k) total += (int64_t)vals[k];
+    *nflag_out = total;
+    *ndeg_out = (int64_t)vals[K];
+    *nnc_out = (int64_t)vals[K + 1];
+    ctx->n_guard_total += (int64_t)vals[K + 2];
+    *minphi_out = -vals[K + 3];
+    cs->count = base;
+    if (append && total > 0 && *ndeg_out == 0 && base + total <= cs->capacity) {
+        if (ds->rank >= 0) {  // this rank's rows at their offset, then every rank's rows everywhere
+            int64_t pre = 0;
+            for (int k = 0; k < ds->rank; ++k) pre += (int64_t)vals[k];
+            cs->count = base + pre;
+            CKS(append_flagged(ctx, cs, gen, (int64_t)vals[ds->rank]));
+            for (int k = 0; k < K; ++k) cnt[k] = (int64_t)vals[k];
+            cs->count = base;
+            if (ds->exchange) CKS(ds->exchange(ds->user, cs, base, cnt.data()));
+        }
+        cs->count = base + total;
+    }
+    ctx->pair_lo = 0;
+    ctx->pair_n = -1;
+    return RELCP_OK;
+}
+
 // a1-a3 with a given U_free (device, nb x 6) already in ctx->ufree.
-static int generate_impl(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, int64_t *n_out) {
+static int generate_impl(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, int64_t *n_out,
+                         const DistSpec *ds = nullptr) {
     const int64_t nb = b->n;
     CKS(ensure_common(ctx, nb));
     k_radius<<<grid_for(nb), RELCP_NT, 0, ctx->stream>>>(nb, b->axes, b->shape, ctx->rad.p);
@@ -301,10 +404,11 @@ static int generate_impl(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraint
     ctx->margin = ctx->p.cutoff > 0.0 ? ctx->p.cutoff : 1e-3;
     CKS(geo_broadphase(ctx, nb, b->pos, ctx->rad.p, ctx->margin));
     PHASE(ctx, "gen.broadphase");
-    int nflag;
+    int64_t nflag;
     double minphi;
     int64_t ndeg, nnc;
-    CKS(snsd_flag_scan(ctx, b->pos, b->shape, b->axes, ctx->p.cutoff, &nflag, &minphi, &ndeg, &nnc));
+    cs->count = 0;
+    CKS(flag_append(ctx, b->pos, b->shape, b->axes, ctx->p.cutoff, cs, 0, true, ds, &nflag, &minphi, &ndeg, &nnc));
     ctx->step_nb = nb;
     ctx->step_pos_key = b->pos;
     ctx->op_nc = -1;
@@ -312,11 +416,9 @@ static int generate_impl(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraint
     if (ndeg > 0) return set_err(ctx, RELCP_E_DEGENERATE, "generate: %lld pairs with coincident centres", (long long)ndeg);
     if (nflag > cs->capacity) {
         cs->count = nflag;
-        return set_err(ctx, RELCP_E_CAPACITY, "generate: %d rows needed, capacity %lld", nflag,
+        return set_err(ctx, RELCP_E_CAPACITY, "generate: %lld rows needed, capacity %lld", (long long)nflag,
                        (long long)cs->capacity);
     }
-    cs->count = 0;
-    CKS(append_flagged(ctx, cs, 0, nflag));
     cs->count = nflag;
     // q_0 = Phi_0 + dt row . U_free   (Phi~_0)
     CKS(op_row_dot_U(ctx, cs, 0, nflag, ctx->ufree.p, ctx->p.dt, cs->q));
@@ -328,7 +430,7 @@ static int generate_impl(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraint
 
 // a7-a8 for the current store; Uc = W D lambda computed here.
 static int check_impl(relcp_ctx *ctx, const relcp_bodies *Ck, relcp_constraints *cs, int gen, int allow_append,
-                      int64_t *n_app, double *min_phi) {
+                      int64_t *n_app, double *min_phi, const DistSpec *ds = nullptr) {
     const int64_t nb = Ck->n;
     if (ctx->step_nb != nb || ctx->step_pos_key != Ck->pos)
         return set_err(ctx, RELCP_E_STATE, "check_and_augment: call relcp_generate_contacts on these bodies first");
@@ -360,23 +462,22 @@ static int check_impl(relcp_ctx *ctx, const relcp_bodies *Ck, relcp_constraints 
     PHASE(ctx, "chk.broadphase");
     CKS(geo_shape_matrices(ctx, nb, ctx->qtrial.p, Ck->axes, Ck->shape, ctx->Sig.p));
     PHASE(ctx, "chk.shape");
-    int nflag;
+    int64_t nflag;
     double minphi;
     int64_t ndeg, nnc;
-    CKS(snsd_flag_scan(ctx, ctx->ptrial.p, Ck->shape, Ck->axes, -ctx->p.eps_ncp, &nflag, &minphi, &ndeg, &nnc));
+    const int64_t base = cs->count;
+    CKS(flag_append(ctx, ctx->ptrial.p, Ck->shape, Ck->axes, -ctx->p.eps_ncp, cs, gen, allow_append != 0, ds, &nflag,
+                    &minphi, &ndeg, &nnc));
     ctx->snsd_nonconv_total += nnc;
     if (min_phi) *min_phi = minphi;
     if (n_app) *n_app = nflag;
     if (ndeg > 0) return set_err(ctx, RELCP_E_DEGENERATE, "check: %lld pairs with coincident centres", (long long)ndeg);
     if (!allow_append || nflag == 0) return nnc > 0 ? RELCP_W_SNSD_NONCONV : RELCP_OK;
-    if (cs->count + nflag > cs->capacity) {
-        cs->count = cs->count + nflag;
+    if (base + nflag > cs->capacity) {
+        cs->count = base + nflag;
         return set_err(ctx, RELCP_E_CAPACITY, "augment: %lld rows needed, capacity %lld", (long long)cs->count,
                        (long long)cs->capacity);
     }
-    const int64_t base = cs->count;
-    CKS(append_flagged(ctx, cs, gen, nflag));
-    cs->count = base + nflag;
     PHASE(ctx, "chk.append");
     // q_new = Phi(C_n) - s row . (W D lambda)   (b_n = A_n iota(x) - Phi~)
     CKS(op_row_dot_U(ctx, cs, base, base + nflag, ctx->U.p, -op_s(ctx), cs->q));
@@ -594,7 +695,8 @@ int relcp_check_and_augment(relcp_ctx *ctx, const relcp_bodies *Ck, relcp_constr
 // Algorithm 1 on one body labelling; relcp_step wraps it with the
 // internal body order (order.cu)
 static int step_core(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_constraints *cs,
-                     relcp_step_report *rep, relcp_solve_cb solve = nullptr, void *user = nullptr) {
+                     relcp_step_report *rep, relcp_solve_cb solve = nullptr, void *user = nullptr,
+                     const DistSpec *ds = nullptr) {
     relcp_step_report R;
     memset(&R, 0, sizeof(R));
     const int64_t nb = b->n;
@@ -610,7 +712,7 @@ static int step_core(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp
     PHASE(ctx, "step.W_ufree");
     int64_t n0 = 0;
     nvtxRangePushA("relcp_generate");
-    int rc = generate_impl(ctx, b, cs, &n0);  // Alg. 1 lines 1-2
+    int rc = generate_impl(ctx, b, cs, &n0, ds);  // Alg. 1 lines 1-2
     nvtxRangePop();
     if (rc < 0) return rc;
     int warn = rc;
@@ -641,7 +743,7 @@ static int step_core(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp
         double minphi = INFINITY;
         const int allow = recursion < ctx->p.max_recursions;
         nvtxRangePushA("relcp_check_and_augment");
-        rc = check_impl(ctx, b, cs, recursion + 1, allow, &napp, &minphi);
+        rc = check_impl(ctx, b, cs, recursion + 1, allow, &napp, &minphi, ds);
         nvtxRangePop();
         R.ms_check += now_ms() - tc;
         if (rc < 0) return rc;
@@ -676,12 +778,12 @@ static int step_core(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp
 // Algorithm 1 in the caller's body order with another LCP solver (the
 // domain-decomposed solve, dd.cu relcp_dd_step)
 int step_entry(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_constraints *cs, relcp_step_report *rep,
-               relcp_solve_cb solve, void *user) {
+               relcp_solve_cb solve, void *user, const DistSpec *ds) {
     CKS(check_views(ctx, b, cs));
     if (!cs->g) return set_err(ctx, RELCP_E_ARG, "step: constraints.g is required");
     if (ctx->p.dynamics == RELCP_INERTIAL && !b->vel) return set_err(ctx, RELCP_E_ARG, "step: inertial needs vel");
     ctx->pairs_internal = 0;
-    return step_core(ctx, b, f_ext, cs, rep, solve, user);
+    return step_core(ctx, b, f_ext, cs, rep, solve, user, ds);
 }
 
 extern "C" {

@@ -195,6 +195,7 @@ struct relcp_ctx {
     DevBuf<long long> scan_tmp;
     DevBuf<int> cell_count, cell_start, cell_fill, cell_items, body_cell;
     DevBuf<long long> pair_cnt;  // per body pair counts (then offsets)
+    int64_t pair_lo = 0, pair_n = -1;  // SNSD / append over pairs [pair_lo, pair_lo + pair_n) (-1: all)
     int bp_cap = 0;              // slot-row capacity of the single-pass broadphase (0: two-pass)
     DevBuf<int> bp_tmp;          // (nb, bp_cap) slot rows
     DevBuf<double> red;          // small reduction buffer
@@ -307,8 +308,23 @@ int lcp_solve(relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs, relc
 // solves delegated to `solve` (dd.cu relcp_dd_step)
 typedef int (*relcp_solve_cb)(void *user, relcp_ctx *ctx, const relcp_bodies *b, relcp_constraints *cs,
                               relcp_solve_report *rep);
+// Domain-decomposed SNSD of generation and checks (dd.cu relcp_dd_step): the
+// candidate pairs (sorted by i) are split by the owner of i (body ranges
+// off[0..K]); rank < 0: every part here, in part order (VIRTUAL); rank >= 0:
+// this rank's part, then `reduce` sums / mins the statistics over the ranks
+// (vals: [0..K) flagged rows per part (this rank's entry set, others 0), K: sum
+// of degenerate pairs, K+1: non-certified, K+2: guard band, K+3: -min Phi) and
+// `exchange` places every rank's appended rows at their offsets.
+struct DistSpec {
+    int K = 1;
+    const int64_t *off = nullptr;
+    int rank = -1;
+    int (*reduce)(void *user, double *vals, int n) = nullptr;
+    int (*exchange)(void *user, relcp_constraints *cs, int64_t base, const int64_t *cnt) = nullptr;
+    void *user = nullptr;
+};
 int step_entry(relcp_ctx *ctx, relcp_bodies *b, const double *f_ext, relcp_constraints *cs, relcp_step_report *rep,
-               relcp_solve_cb solve, void *user);
+               relcp_solve_cb solve, void *user, const DistSpec *dist = nullptr);
 // split-reduction pieces of the BB solve for the domain-decomposed solve (dd.cu):
 // each writes its part's block-reduced partials to acc_out (device) instead of
 // finalizing; lcp_dd_finalize applies the finalize step of `kind` to ctx->st

@@ -716,12 +716,14 @@ extern "C" int relcp_dd_solve_lcp(relcp_dd *dd, relcp_constraints *cs, relcp_sol
 
 // ------------------------------------------------------------ domain-decomposed ReLCP step
 // Algorithm 1 with every LCP solve distributed (relcp_dd_solve_lcp
-// on the store of the current recursion) and generation / checks / augmentation
-// replicated on every rank (each rank holds all body states; the step's
-// bitwise-deterministic single-domain kernels give every rank the same
-// store).  NCCL: after each solve every rank sends its rows' lambda and g to
-// every other rank (grouped send / recv), so the replicated check sees the
-// whole solution.
+// on the store of the current recursion) and the SNSD of generation and checks
+// split by the owner of i (each rank scans the candidate pairs of its bodies;
+// the broadphase, trial configuration, q and the store merge stay replicated:
+// every rank holds all body states and, after the exchanges, the same store).
+// NCCL: after each SNSD phase the ranks all-reduce the counts / statistics and
+// exchange their appended rows; after each solve their rows' lambda and g
+// (grouped send / recv), so the replicated check sees the whole solution
+// (DESIGN.md §8).
 static int dd_allgather_rows(relcp_dd *dd, relcp_constraints *cs) {
     DDCTX;
     if (dd->rank < 0 || dd->K == 1) return RELCP_OK;
@@ -753,10 +755,74 @@ static int dd_step_solve(void *user, relcp_ctx *ctx, const relcp_bodies *b, relc
     return rg < 0 ? rg : rc;
 }
 
+// the SNSD phases split by the owner of i (DistSpec, abi.cu flag_append): the
+// statistics of every rank summed (counts, degenerate, non-certified, guard
+// band) and max-reduced (-min Phi) in two all-reduces
+static int dd_reduce_stats(void *user, double *vals, int n) {
+    relcp_dd *dd = (relcp_dd *)user;
+    DDCTX;
+    DevBuf<double> d;
+    CK(d.grow(n));
+    CK(cudaMemcpyAsync(d.p, vals, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    CKS(nccl_check(dd, g_nccl.AllReduce(d.p, d.p, n - 1, ncclDouble_, ncclSum_, dd->comm, ctx->stream),
+                   "ncclAllReduce"));
+    CKS(nccl_check(dd, g_nccl.AllReduce(d.p + n - 1, d.p + n - 1, 1, ncclDouble_, ncclMax_, dd->comm, ctx->stream),
+                   "ncclAllReduce"));
+    CK(cudaMemcpyAsync(vals, d.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return RELCP_OK;
+}
+
+// every rank's appended rows [base + pre_q, base + pre_q + cnt[q]) of every
+// store plane to every other rank (grouped send / recv)
+static int dd_exchange_rows(void *user, relcp_constraints *cs, int64_t base, const int64_t *cnt) {
+    relcp_dd *dd = (relcp_dd *)user;
+    DDCTX;
+    const int K = dd->K, me = dd->rank;
+    std::vector<int64_t> pre(K + 1, 0);
+    for (int q = 0; q < K; ++q) pre[q + 1] = pre[q] + cnt[q];
+    const int64_t cap = cs->capacity;
+    struct Plane {
+        void *p;
+        int esz;
+    };
+    std::vector<Plane> planes = {{cs->ia, 4}, {cs->ib, 4}, {cs->gen, 4}, {cs->phi, 8}, {cs->q, 8}, {cs->lambda, 8}};
+    for (int k = 0; k < 3; ++k) {
+        planes.push_back({cs->n + k * cap, 8});
+        planes.push_back({cs->ta + k * cap, 8});
+        planes.push_back({cs->tb + k * cap, 8});
+    }
+    CKS(nccl_check(dd, g_nccl.GroupStart(), "ncclGroupStart"));
+    for (const Plane &pl : planes) {
+        char *p = (char *)pl.p;
+        if (!p) continue;
+        const int esz = pl.esz;
+        for (int q = 0; q < K; ++q) {
+            if (q == me) continue;
+            // ncclInt32 = 2 for 4-byte planes, ncclDouble = 8
+            const int dt = esz == 4 ? 2 : ncclDouble_;
+            if (cnt[me]) CKS(nccl_check(dd, g_nccl.Send(p + esz * (base + pre[me]), cnt[me], dt, q, dd->comm,
+                                                        ctx->stream), "ncclSend"));
+            if (cnt[q]) CKS(nccl_check(dd, g_nccl.Recv(p + esz * (base + pre[q]), cnt[q], dt, q, dd->comm,
+                                                       ctx->stream), "ncclRecv"));
+        }
+    }
+    CKS(nccl_check(dd, g_nccl.GroupEnd(), "ncclGroupEnd"));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return RELCP_OK;
+}
+
 extern "C" int relcp_dd_step(relcp_dd *dd, relcp_bodies *b, const double *f_ext, relcp_constraints *cs,
                              relcp_step_report *rep) {
     if (!dd) return RELCP_E_ARG;
     DDCTX;
     if (!b || dd->off[dd->K] != b->n) return set_err(ctx, RELCP_E_ARG, "dd_step: part offsets must end at n bodies");
-    return step_entry(ctx, b, f_ext, cs, rep, dd_step_solve, dd);
+    DistSpec ds;
+    ds.K = dd->K;
+    ds.off = dd->off.data();
+    ds.rank = dd->rank;
+    ds.reduce = dd_reduce_stats;
+    ds.exchange = dd_exchange_rows;
+    ds.user = dd;
+    return step_entry(ctx, b, f_ext, cs, rep, dd_step_solve, dd, &ds);
 }

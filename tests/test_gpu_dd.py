@@ -1,4 +1,4 @@
-"""Domain-decomposed Delassus apply and BB solve (SURVEY §8(e) / §8(f) rank 4,
+"""Domain-decomposed Delassus apply, BB solve and ReLCP step (SURVEY §8(e) / §8(f) rank 4,
 DESIGN.md §8) on one GPU as K virtual parts (halo exchange by device copies),
 and the NCCL transport at world size 1, against the CPU oracle:
 
@@ -221,9 +221,22 @@ def _dd_step_vs_oracle(orc, R, sc, K, max_recursions, rank=-1, uid=None):
 
 @pytest.mark.parametrize("K", [1, 2, 3])
 def test_dd_step_cfg5_recipe(orc, R, K):
-    """The bench workload's recipe at 1000 bodies, two augmentations."""
-    rep, _, _ = _dd_step_vs_oracle(orc, R, scenes.cfg5(n=1000), K, max_recursions=2)
+    """The bench workload's recipe at 1000 bodies, two augmentations.  The
+    generation's SNSD runs split by the owner of i (DistSpec): the A_0 rows
+    (gen 0, found at C^k before any solve) are bitwise the single-domain
+    step's."""
+    sc = scenes.cfg5(n=1000)
+    rep, _, cs = _dd_step_vs_oracle(orc, R, sc, K, max_recursions=2)
     assert rep["recursions"] == 2
+    ctx = R.Context(dynamics=sc["dynamics"], dt=sc["dt"], box=list(sc["box"]), cutoff=sc["cutoff"],
+                    eps_ncp=sc["eps_ncp"], lcp_tol=1e-12, lcp_max_iter=2_000_000, max_recursions=2)
+    b1 = R.BodyState.from_scene(sc)
+    c1 = R.ConstraintStore(cs.capacity)
+    ctx.step(b1, c1)
+    g1, g2 = c1.to_numpy(), cs.to_numpy()
+    m1, m2 = g1["gen"] == 0, g2["gen"] == 0
+    for k in ("ia", "ib", "n", "ta", "tb", "phi"):
+        assert np.array_equal(g1[k][m1], g2[k][m2]), k
 
 
 @pytest.mark.parametrize("K", [2, 4])
