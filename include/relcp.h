@@ -108,7 +108,15 @@ typedef struct relcp_params {
                              the TMA-staged pipeline over per-group records
                              (k6pipe.cuh; bitwise equal to the per-warp kernel,
                              measured 3.1x slower) [0]          */
+    int32_t k6_bpw;       /* bodies per warp of the CSR K6 on sorted stores:
+                             0 = auto [default: RELCP_K6_BPW_SMALL for N <=
+                             RELCP_K6_SMALL_N bodies, else 32], or 8 / 16 / 32.
+                             Each body's summation order does not depend on it
+                             (bitwise identical results).      */
 } relcp_params;
+
+#define RELCP_K6_SMALL_N 65536
+#define RELCP_K6_BPW_SMALL 8
 
 #define RELCP_REORDER_OFF 0
 #define RELCP_REORDER_AUTO 1

@@ -36,6 +36,7 @@ static int check_params(const relcp_params *p) {
         return 0;
     if (p->reorder < RELCP_REORDER_OFF || p->reorder > RELCP_REORDER_ON) return 0;
     if (p->layout < RELCP_LAYOUT_CSR || p->layout > RELCP_LAYOUT_AUTO) return 0;
+    if (p->k6_bpw != 0 && p->k6_bpw != 8 && p->k6_bpw != 16 && p->k6_bpw != 32) return 0;
     return 1;
 }
 
@@ -512,6 +513,7 @@ void relcp_default_params(relcp_params *p) {
     p->cluster = 1;
     p->snsd_cert = 1;
     p->k6_pipe = 0;
+    p->k6_bpw = 0;
 }
 
 int relcp_create(relcp_ctx **out, const relcp_params *p, void *cuda_stream) {

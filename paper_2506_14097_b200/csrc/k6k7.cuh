@@ -93,15 +93,22 @@ __device__ __forceinline__ double xeff_at(const XEff &e, int c) {
 // bitwise deterministic), then U_b = W_b F_b is stored through a shared-memory
 // transpose (coalesced).  Fout: the raw sums F_b; Fa (MODE 3): a-side sums
 // formed by the fused row pass.
-template <int MODE, bool SORTED>
+//
+// GB (bodies per warp, 32 / 16 / 8): lanes 0..GB-1 own bodies GB w .. GB w +
+// GB - 1; all 32 lanes stream the tiles.  Each body's summation order does not
+// depend on GB (bitwise identical U), only the number of dependent tile
+// round trips per warp does: small stores (few groups per SM) run GB < 32 so
+// that a warp's chain covers fewer entries and more warps are in flight.
+template <int MODE, bool SORTED, int GB = 32>
 __device__ __forceinline__ void k6_group(int64_t w, const K6Op &o, const XEff &xe, double2 (*c6)[SCATTER_TILE + 1],
                                          int lane, double *__restrict__ U, double *__restrict__ Fout,
                                          const double *__restrict__ Fa) {
+    static_assert(GB == 32 || GB == 16 || GB == 8, "bodies per warp");
     const int64_t nb = o.nb;
-    const int64_t b0 = w << 5;
+    const int64_t b0 = w * GB;
     const int64_t b = b0 + lane;
-    const bool own = b < nb;
-    const int last = nb - b0 < 32 ? (int)(nb - b0 - 1) : 31;
+    const bool own = lane < GB && b < nb;
+    const int last = nb - b0 < GB ? (int)(nb - b0 - 1) : GB - 1;
     double f[6] = {0, 0, 0, 0, 0, 0};
     // stream [e0, e1) of the warp in coalesced tiles; lane sums its [s, t)
     auto tiles = [&](int s, int t, auto &&fetch) {
@@ -176,7 +183,7 @@ __device__ __forceinline__ void k6_group(int64_t w, const K6Op &o, const XEff &x
     __syncwarp();
     const int64_t nvals = 6 * (int64_t)(last + 1);
 #pragma unroll
-    for (int i = 0; i < 6; ++i) {
+    for (int i = 0; i < (6 * GB + 31) / 32; ++i) {
         const int m = lane + 32 * i;
         if (m < nvals) {
             U[6 * b0 + m] = flat[m];

@@ -391,7 +391,7 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
 // MODE: 0 apply (x_eff = x), 1 BB step (x_eff = max(0, x - alpha g)),
 // 2 APGD step (y = x + beta (x - x'), g_y likewise, x_eff = max(0, y - t g_y);
 // (x, g) / (x', g') are (x, g) / (xb, gb) or swapped by the device parity bit).
-template <int MODE, bool SORTED>
+template <int MODE, bool SORTED, int GB = 32>
 __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
     K6Op o, const double *__restrict__ x, const double *__restrict__ g, const double *__restrict__ xb,
     const double *__restrict__ gb, const LcpState *__restrict__ st, const double *__restrict__ xscale,
@@ -404,13 +404,14 @@ __global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
     if (MODE != 0 && st->done) return;
     const XEff xe = xeff_setup<MODE>(st, x, g, xb, gb, xscale);
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-    const int64_t nwarp = (o.nb + 31) >> 5;
+    const int64_t nwarp = (o.nb + GB - 1) / GB;
     for (int64_t wi = blockIdx.x * (int64_t)SCATTER_WPB + wl; wi < nwarp; wi += (int64_t)gridDim.x * SCATTER_WPB) {
         // K6_REVERSE: sweep bodies high -> low, so K6 starts on the rows, x and g
         // K7 (ascending) touched last (still in L2) and ends on the bodies whose
         // U / rows K7 touches first
         const int64_t w = K6_REVERSE ? nwarp - 1 - wi : wi;
-        k6_group<MODE, SORTED>(w, o, xe, reinterpret_cast<double2(*)[SCATTER_TILE + 1]>(sm[wl]), lane, U, Fout, Fa);
+        k6_group<MODE, SORTED, GB>(w, o, xe, reinterpret_cast<double2(*)[SCATTER_TILE + 1]>(sm[wl]), lane, U, Fout,
+                                   Fa);
     }
 }
 
@@ -657,7 +658,13 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
         return RELCP_OK;
     }
     const int64_t E = ctx->op_sorted ? ctx->op_nc : 2 * ctx->op_nc;
-    const int64_t nwarp = (nb + 31) / 32;
+    // bodies per warp (params.k6_bpw): 32, or RELCP_K6_BPW_SMALL for stores with
+    // few 32-body groups per SM, where the per-warp chain of dependent tile
+    // loads is the floor (same-box A/B, profiles/README: cfg2 iteration 14.6 ->
+    // 13.2 us with 8; cfg5 A_0 loses with 8 or 16: 0.28 -> 0.38 / 0.30 ms)
+    int bpw = ctx->p.k6_bpw ? ctx->p.k6_bpw : (nb <= RELCP_K6_SMALL_N ? RELCP_K6_BPW_SMALL : 32);
+    if (!ctx->op_sorted) bpw = 32;
+    const int64_t nwarp = (nb + bpw - 1) / bpw;
     int64_t grid = (nwarp + SCATTER_WPB - 1) / SCATTER_WPB;
     if (grid > (int64_t)RELCP_SM_COUNT * SCATTER_MINB * SCATTER_WAVES)
         grid = (int64_t)RELCP_SM_COUNT * SCATTER_MINB * SCATTER_WAVES;
@@ -671,6 +678,14 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
     if (mode == 3) {
         if (!ctx->op_sorted) return set_err(ctx, RELCP_E_STATE, "fused solver needs a store sorted by ia");
         k_scatter<3, true><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+    } else if (ctx->op_sorted && bpw == 8) {
+        if (mode == 1) CK(launch_k(ctx->pdl, k_scatter<1, true, 8>, G, T, 0, ctx->stream, SCATTER_ARGS));
+        else if (mode == 2) CK(launch_k(ctx->pdl, k_scatter<2, true, 8>, G, T, 0, ctx->stream, SCATTER_ARGS));
+        else k_scatter<0, true, 8><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
+    } else if (ctx->op_sorted && bpw == 16) {
+        if (mode == 1) CK(launch_k(ctx->pdl, k_scatter<1, true, 16>, G, T, 0, ctx->stream, SCATTER_ARGS));
+        else if (mode == 2) CK(launch_k(ctx->pdl, k_scatter<2, true, 16>, G, T, 0, ctx->stream, SCATTER_ARGS));
+        else k_scatter<0, true, 16><<<G, T, 0, ctx->stream>>>(SCATTER_ARGS);
     } else if (ctx->op_sorted) {
         if (mode == 1) CK(launch_k(ctx->pdl, k_scatter<1, true>, G, T, 0, ctx->stream, SCATTER_ARGS));
         else if (mode == 2) CK(launch_k(ctx->pdl, k_scatter<2, true>, G, T, 0, ctx->stream, SCATTER_ARGS));

@@ -40,7 +40,7 @@ class Params(ctypes.Structure):
                 ("lcp_tol", f64), ("lcp_max_iter", i64), ("check_every", i32), ("power_iters", i32),
                 ("box", f64 * 3), ("xi", f64), ("n_dirs", i32), ("solver", i32), ("reorder", i32),
                 ("layout", i32), ("cluster", i32), ("snsd_cert", i32),
-                ("k6_pipe", i32)]
+                ("k6_pipe", i32), ("k6_bpw", i32)]
 
 
 SOLVER_BB, SOLVER_APGD, SOLVER_APGD_FUSED = 0, 1, 2

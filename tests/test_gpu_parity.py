@@ -760,3 +760,52 @@ def test_k6_pipe_bitwise(orc, R, hubs, dynamics):
     for a, c in zip(out[0][:5], out[1][:5]):
         assert torch.equal(a, c)
     assert out[0][5] == out[1][5] == 40
+
+
+@pytest.mark.parametrize("nb,hubs", [(20_000, False), (20_000, True), (70_000, False)])
+def test_k6_bodies_per_warp_bitwise(orc, R, nb, hubs):
+    """K6 with 8, 16 or 32 bodies per warp (params.k6_bpw; auto = 8 up to
+    RELCP_K6_SMALL_N bodies) forms every body's sum in the same
+    order: apply, wrench and a fixed number of BB iterations are bitwise equal
+    across the three, and the apply matches the oracle at 1e-12.  hubs: bodies
+    with 300-700 rows (many tiles in one warp); ragged last group (nb % 32)."""
+    nb += 13
+    nc = 3 * nb
+    b, ia, ib, n, ra, rb = scenes.local_constraint_network(nb, nc, 37, 0)
+    if hubs:
+        rng = np.random.default_rng(6)
+        hi = np.concatenate([np.full(700, 1000), np.full(300, nb - 20)])
+        hj = np.concatenate([rng.integers(1001, nb, 700), rng.integers(nb - 19, nb, 300)])
+        ia, ib = np.concatenate([ia, hi]).astype(np.int32), np.concatenate([ib, hj]).astype(np.int32)
+        n = np.concatenate([n, rng.normal(size=(1000, 3))])
+        n /= np.linalg.norm(n, axis=1, keepdims=True)
+        ra = np.concatenate([ra, rng.uniform(-0.7, 0.7, (1000, 3))])
+        rb = np.concatenate([rb, rng.uniform(-0.7, 0.7, (1000, 3))])
+        o = np.lexsort((ib, ia))
+        ia, ib, n, ra, rb = ia[o], ib[o], n[o], ra[o], rb[o]
+    ta, tb = np.cross(ra, n), np.cross(rb, n)
+    m = len(ia)
+    x = np.random.default_rng(7).standard_normal(m)
+    y_ref = orc.delassus_apply(orc.body_W(b), ia, ib, n, ta, tb, 1e-6, x)
+    bodies = R.BodyState.from_scene(b)
+    xd = torch.as_tensor(x, device="cuda")
+    q = torch.as_tensor(np.random.default_rng(8).standard_normal(m) * 1e-6, device="cuda")
+    out = []
+    for bpw in (8, 16, 32, 0):
+        ctx = _ctx(R, dict(dynamics=0, dt=1e-3, cutoff=0.1, eps_ncp=1e-5, box=[0, 0, 0]), k6_bpw=bpw,
+                   lcp_tol=1e-30, lcp_max_iter=40, layout=0, cluster=0)
+        cs = R.ConstraintStore.from_rows(ia, ib, n, ta, tb)
+        ctx.prepare_operator(bodies, cs)
+        y = torch.empty_like(xd)
+        ctx.delassus_apply(bodies, cs, xd, y, 1e-6)
+        assert np.max(np.abs(y.cpu().numpy() - y_ref)) <= 1e-12 * np.max(np.abs(y_ref))
+        F = torch.empty(nb, 6, dtype=torch.float64, device="cuda")
+        U = torch.empty_like(F)
+        ctx.wrench(bodies, cs, xd, F, U)
+        cs.q[:m] = q
+        rep = ctx.solve_lcp(bodies, cs)
+        out.append((y, F, U, cs.lam[:m].clone(), cs.g[:m].clone(), rep["iterations"]))
+    for o in out[1:]:
+        for a, c in zip(out[0][:5], o[:5]):
+            assert torch.equal(a, c)
+        assert o[5] == 40

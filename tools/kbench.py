@@ -21,7 +21,8 @@ if len(sys.argv) > 3 and sys.argv[3] == "relaxed":
 ctx = R.Context(dynamics=sc["dynamics"], dt=sc["dt"], box=list(sc["box"]), lcp_max_iter=iters, lcp_tol=1e-30,
                 solver=int(os.environ.get("RELCP_SOLVER", "0")),
                 layout=int(os.environ.get("RELCP_LAYOUT", "2")),
-                k6_pipe=int(os.environ.get("RELCP_K6PIPE", "0")))  # 20 power iterations: APGD steps 1/(1.1 L)
+                k6_pipe=int(os.environ.get("RELCP_K6PIPE", "0")),
+                k6_bpw=int(os.environ.get("RELCP_K6_BPW", "0")))  # 20 power iterations: APGD steps 1/(1.1 L)
 bodies = R.BodyState.from_scene(sc)
 cs = R.ConstraintStore(8 * n)
 ctx.generate_contacts(bodies, cs)

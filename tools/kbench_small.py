@@ -14,7 +14,8 @@ name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 2000
 sc = {"cfg1": scenes.cfg1, "cfg2": scenes.cfg2, "cfg3": scenes.cfg3}[name]()
 ctx = R.Context(dynamics=sc["dynamics"], dt=sc["dt"], box=list(sc["box"]), cutoff=sc["cutoff"], lcp_max_iter=iters,
-                lcp_tol=1e-30, cluster=int(os.environ.get("RELCP_CLUSTER", "1")))
+                lcp_tol=1e-30, cluster=int(os.environ.get("RELCP_CLUSTER", "1")),
+                k6_bpw=int(os.environ.get("RELCP_K6_BPW", "0")))
 bodies = R.BodyState.from_scene(sc)
 cs = R.ConstraintStore(8 * sc["n"])
 ctx.generate_contacts(bodies, cs)
