@@ -12,6 +12,9 @@
 #ifndef SCATTER_TILE
 #define SCATTER_TILE 64  // entries staged per warp per tile
 #endif
+#ifndef K6_CL
+#define K6_CL 0  // 1 / 2: component-lane segment sums (k6_group), per-round loops / one merged loop
+#endif
 
 struct V6 {
     double v[6];
@@ -136,13 +139,73 @@ __device__ __forceinline__ void k6_group(int64_t w, const K6Op &o, const XEff &x
             __syncwarp();
         }
     };
+#if K6_CL
+    // Component lanes (K6_CL, GB = 32, MODE != 3): the 192 sums (body, k) of the
+    // group are held one per lane and round, pair p = 32 r + lane = 6 body + k
+    // (the AoS order of U / F).  Entries are staged AoS (6 doubles each,
+    // conflict-free 16-byte stores); a lane adds ONE double per entry of its
+    // pair's body, so a warp-wide shared load serves 32 pairs of ~5 bodies
+    // (8-byte accesses, 2-3 wavefronts) instead of 32 bodies x 16 bytes at
+    // lane-dependent offsets.  Per-pair order = the per-body order above:
+    // bitwise the same sums.
+    constexpr bool CL = GB == 32 && MODE != 3;
+    double *st6 = &c6[0][0].x;
+    auto tiles_cl = [&](int s, int t, auto &&fetch) {
+        const int e0 = __shfl_sync(0xffffffffu, s, 0);
+        const int e1 = __shfl_sync(0xffffffffu, t, last);
+        int sr[6], tr[6];
+#pragma unroll
+        for (int r = 0; r < 6; ++r) {
+            sr[r] = __shfl_sync(0xffffffffu, s, (32 * r + lane) / 6);
+            tr[r] = __shfl_sync(0xffffffffu, t, (32 * r + lane) / 6);
+        }
+        double2 *st2 = reinterpret_cast<double2 *>(st6);
+        for (int base = e0; base < e1; base += SCATTER_TILE) {
+#pragma unroll
+            for (int i = 0; i < SCATTER_TILE / 32; ++i) {
+                const int e = base + lane + 32 * i;
+                if (e < e1) {
+                    const V6 v = fetch(e);
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) st2[3 * (lane + 32 * i) + k] = make_double2(v.v[2 * k], v.v[2 * k + 1]);
+                }
+            }
+            __syncwarp();
+#if K6_CL == 2
+            int lo[6], nn[6], mx = 0;
+#pragma unroll
+            for (int r = 0; r < 6; ++r) {
+                lo[r] = max(sr[r], base) - base;
+                nn[r] = min(tr[r], base + SCATTER_TILE) - base - lo[r];
+                mx = max(mx, nn[r]);
+                lo[r] = 6 * lo[r] + (32 * r + lane) % 6;
+            }
+            for (int jj = 0; jj < mx; ++jj)
+#pragma unroll
+                for (int r = 0; r < 6; ++r)
+                    if (jj < nn[r]) f[r] += st6[lo[r] + 6 * jj];
+#else
+#pragma unroll
+            for (int r = 0; r < 6; ++r) {
+                const int lo = max(sr[r], base) - base, hi = min(tr[r], base + SCATTER_TILE) - base;
+                const double *pr = st6 + (32 * r + lane) % 6;
+                for (int j = lo; j < hi; ++j) f[r] += pr[6 * j];
+            }
+#endif
+            __syncwarp();
+        }
+    };
+#else
+    constexpr bool CL = false;
+    auto tiles_cl = [&](int, int, auto &&) {};
+#endif
     if (MODE == 3) {
         if (own)
 #pragma unroll
             for (int k = 0; k < 6; ++k) f[k] = Fa[k * nb + b];
     } else if (SORTED) {
         const int sa = own ? o.pa[b] : 0, ta_ = own ? o.pa[b + 1] : 0;
-        tiles(sa, ta_, [&](int e) {
+        auto fa = [&](int e) {
             const double xv = xeff_at<MODE>(xe, e);
             V6 v;
 #pragma unroll
@@ -151,16 +214,29 @@ __device__ __forceinline__ void k6_group(int64_t w, const K6Op &o, const XEff &x
                 v.v[3 + k] = -o.cta[k * o.cap + e] * xv;
             }
             return v;
-        });
+        };
+        if (CL) tiles_cl(sa, ta_, fa);
+        else tiles(sa, ta_, fa);
     }
     const int s = own ? o.row_ptr[b] : 0, t = own ? o.row_ptr[b + 1] : 0;
-    tiles(s, t, [&](int e) {
+    auto fb = [&](int e) {
         const double xv = xeff_at<MODE>(xe, o.ecid[e]);
         V6 v;
 #pragma unroll
         for (int k = 0; k < 6; ++k) v.v[k] = o.ew[k * o.E + e] * xv;
         return v;
-    });
+    };
+    if (CL) tiles_cl(s, t, fb);
+    else tiles(s, t, fb);
+    double *flat = &c6[0][0].x;  // 3 * 65 double2 >= 2 * 192 doubles
+    if (CL) {  // pair sums -> the owning lane's f[0..5]
+#pragma unroll
+        for (int r = 0; r < 6; ++r) flat[192 + 32 * r + lane] = f[r];
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 6; ++k) f[k] = flat[192 + 6 * lane + k];
+        __syncwarp();
+    }
     // U_b = W_b F_b ; staged through shared memory for a coalesced AoS store
     const double *W = o.W;
     double u[6] = {0, 0, 0, 0, 0, 0};
@@ -174,7 +250,6 @@ __device__ __forceinline__ void k6_group(int64_t w, const K6Op &o, const XEff &x
         u[4] = s01 * f[3] + s11 * f[4] + s12 * f[5];
         u[5] = s02 * f[3] + s12 * f[4] + s22 * f[5];
     }
-    double *flat = &c6[0][0].x;  // 3 * 65 double2 >= 2 * 192 doubles
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
         flat[6 * lane + k] = u[k];
