@@ -25,15 +25,26 @@
 #define ITER_MINB 4  // resident K7 blocks per SM (register budget); grid = 148 * ITER_MINB
 #endif
 #ifndef ITER_MINB_CR
-#define ITER_MINB_CR 2  // with compact rows (decode registers, 128 per thread): same-box A/B, round 2
-#endif                  // (K7 on the relaxed cfg5 store / cfg3 iteration): ILP 3 x 2 blocks 153 us / 31.0 us,
-                        // ILP 4 x 2 165 / 32.4, ILP 2 x 3 168 / 34.9, ILP 1 x 4 163 / 37.5, ILP 5-6 x 2 181-195
+#define ITER_MINB_CR 3  // K7 with compact rows: 1 row per thread and trip x 3 blocks of 256 (80 registers, 24
+#endif                  // warps per SM).  Same-box A/B, K7 on cfg5 A_0 / the relaxed cfg5 store (us): ILP 1 x 3
+                        // blocks 111.0 / 146.5; ILP 3 x 2 (round-2 default until the last session) 116.2 / 153.5;
+                        // ILP 1 x 4 x 192 threads 111.3 / 146.7, 1 x 6 x 128 112.0 / 147.4, 1 x 5 x 128 (96 regs)
+                        // 114.5 / 150.6, 1 x 7 x 128 115.3 / 151.5, 1 x 4 x 256 (64 regs, spills) 124.9 / 164.3,
+                        // 2 x 3 127.2 / 168.6, 2 x 2 116.2 / 154.5, 4 x 2 139.5 / 186.4; ids one trip ahead
+                        // (K7_IDPRE) +4 %.  cfg3 iteration 31.6 -> 31.7 us, cfg2 18.8 -> 18.0 us.
+#ifndef APGD_MINB_CR
+#define APGD_MINB_CR 2  // k_apgd_iter keeps 128 registers
+#endif
 #ifndef ITER_ILP_CR
-#define ITER_ILP_CR 3
+#define ITER_ILP_CR 1
 #endif
 #ifndef ITER_ILP
 #define ITER_ILP 2   // rows per thread per trip in K7
 #endif
+#ifndef ITER_NT_CR
+#define ITER_NT_CR RELCP_NT  // threads per K7 block with compact rows
+#endif
+#define K7_NT(CR) ((CR) ? ITER_NT_CR : RELCP_NT)
 
 __global__ void k_project(int64_t nc, double *x) {
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x)
@@ -174,7 +185,7 @@ __device__ void bb_iter_finalize(LcpState *st, const double *acc) {
 // slots and form x_k + t (x+ - x_k), g_k + t (g+ - g_k) on the fly (A is
 // linear), so the common t = 1 iteration moves exactly the bytes of plain BB.
 template <bool CR>
-__global__ void __launch_bounds__(RELCP_NT, CR ? ITER_MINB_CR : ITER_MINB) k_lcp_iter(int64_t nc, int64_t cap, const int32_t *__restrict__ ia,
+__global__ void __launch_bounds__(K7_NT(CR), CR ? ITER_MINB_CR : ITER_MINB) k_lcp_iter(int64_t nc, int64_t cap, const int32_t *__restrict__ ia,
                                                        const int32_t *__restrict__ ib, const double *__restrict__ n,
                                                        const double *__restrict__ ta, const double *__restrict__ tb,
                                                        int64_t rs, const double *__restrict__ rc,
@@ -252,7 +263,7 @@ __global__ void __launch_bounds__(RELCP_NT) k_bb_finish(int64_t nc, double *x, d
 //   beta+  = theta (1 - theta) / (theta^2 + theta+).
 // The new iterate overwrites the previous one's slot; the parity bit flips.
 template <bool CR>
-__global__ void __launch_bounds__(RELCP_NT, CR ? ITER_MINB_CR : ITER_MINB) k_apgd_iter(
+__global__ void __launch_bounds__(RELCP_NT, CR ? APGD_MINB_CR : ITER_MINB) k_apgd_iter(
     int64_t nc, int64_t cap, const int32_t *__restrict__ ia, const int32_t *__restrict__ ib,
     const double *__restrict__ n, const double *__restrict__ ta, const double *__restrict__ tb, int64_t rs,
     const double *__restrict__ rc, const double *__restrict__ U, double s, const double *__restrict__ q, double *xA, double *gA, double *xB,
@@ -586,7 +597,8 @@ static int lcp_solve_view(relcp_ctx *ctx, const relcp_bodies *b, relcp_constrain
     // g_0 = A x_0 + q
     CKS(op_scatter(ctx, nb, cs->lambda, nullptr, 0, nullptr, ctx->U.p, nullptr, nullptr, nullptr, sl));
     const bool cr = ctx->op_compact != 0;
-    const int gridi = cr ? grid_for(nc, RELCP_NT, ITER_MINB_CR) : gridc;  // iteration kernels: one wave
+    const int gridi = cr ? grid_for(nc, RELCP_NT, APGD_MINB_CR) : gridc;  // k_apgd_iter: one wave
+    const int grid7 = cr ? grid_for(nc, ITER_NT_CR, ITER_MINB_CR) : gridc;  // K7 (k_lcp_iter)
 #define ROWS_ARGS nc, cs->capacity, cs->ia, cs->ib, cs->n, cs->ta, cs->tb, ctx->op_rs, ctx->rc.p
     if (cr)
         k_lcp_init<true><<<gridc, RELCP_NT, 0, st>>>(ROWS_ARGS, ctx->U.p, s, cs->q, cs->lambda, cs->g, ctx->partials.p,
@@ -688,7 +700,7 @@ static int lcp_solve_view(relcp_ctx *ctx, const relcp_bodies *b, relcp_constrain
                 CK(launch_k(ctx->pdl, k_apgd_iter<false>, gridi, RELCP_NT, 0, st, ROWS_ARGS, ctx->U.p, s, cs->q,
                             cs->lambda, cs->g, xB, gB, ctx->partials.p, ctx->counter.p, ctx->st.p));
             else if (cr)
-                CK(launch_k(ctx->pdl, k_lcp_iter<true>, gridi, RELCP_NT, 0, st, ROWS_ARGS, ctx->U.p, s, cs->q,
+                CK(launch_k(ctx->pdl, k_lcp_iter<true>, grid7, ITER_NT_CR, 0, st, ROWS_ARGS, ctx->U.p, s, cs->q,
                             cs->lambda, cs->g, xB, gB, ctx->partials.p, ctx->counter.p, ctx->st.p, (double *)nullptr));
             else
                 CK(launch_k(ctx->pdl, k_lcp_iter<false>, gridi, RELCP_NT, 0, st, ROWS_ARGS, ctx->U.p, s, cs->q,
@@ -863,7 +875,7 @@ int lcp_dd_init(relcp_ctx *ctx, const relcp_constraints *cs, double s, double *a
 int lcp_dd_iter(relcp_ctx *ctx, const relcp_constraints *cs, double s, double *xB, double *gB, double *acc_out) {
     const int64_t nc = cs->count;
     if (ctx->op_compact)
-        k_lcp_iter<true><<<grid_for(nc, RELCP_NT, ITER_MINB_CR), RELCP_NT, 0, ctx->stream>>>(
+        k_lcp_iter<true><<<grid_for(nc, ITER_NT_CR, ITER_MINB_CR), ITER_NT_CR, 0, ctx->stream>>>(
             DD_ROWS, ctx->U.p, s, cs->q, cs->lambda, cs->g, xB, gB, ctx->partials.p, ctx->counter.p, ctx->st.p,
             acc_out);
     else
