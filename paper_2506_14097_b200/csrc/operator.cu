@@ -49,6 +49,13 @@
 #ifndef SCATTER_MINB
 #define SCATTER_MINB 8   // resident blocks per SM the register budget must allow (64 regs at 4 warps)
 #endif
+#ifndef SCATTER_MINB32
+#define SCATTER_MINB32 9  // the same for the 32-bodies-per-warp CSR kernel (large stores): 56 registers, 36 warps
+#endif                    // per SM.  Same-box A/B, BB K6 on cfg5 A_0 / the relaxed cfg5 store (us): 4 warps x 8
+                          // blocks (64 regs) 173.4 / 212.7; 4 x 9 162.7 / 198.7; 3 x 11 161.7 / 198.1; 3 x 12
+                          // 161.9 / 197.9; 2 x 18 161.0 / 197.3; 6 x 6 165.3 / 201.2; 5 x 7 166.0 / 203.4 (all
+                          // 56 regs); 3 x 10 and 5 x 6 (64 regs, 30 warps) 176.7 / 217.7 and 179.4 / 219.9.
+                          // The 8- / 16-body kernels of the small stores keep 8 blocks (cfg2 18.0 vs 18.5 us).
 
 // ------------------------------------------------------------ W blocks (SoA planes)
 __global__ void k_build_W(int64_t nb, int dyn, double xi, const double *__restrict__ quat,
@@ -392,7 +399,7 @@ int op_prepare(relcp_ctx *ctx, const relcp_bodies *b, const relcp_constraints *c
 // 2 APGD step (y = x + beta (x - x'), g_y likewise, x_eff = max(0, y - t g_y);
 // (x, g) / (x', g') are (x, g) / (xb, gb) or swapped by the device parity bit).
 template <int MODE, bool SORTED, int GB = 32>
-__global__ void __launch_bounds__(32 * SCATTER_WPB, SCATTER_MINB) k_scatter(
+__global__ void __launch_bounds__(32 * SCATTER_WPB, GB == 32 ? SCATTER_MINB32 : SCATTER_MINB) k_scatter(
     K6Op o, const double *__restrict__ x, const double *__restrict__ g, const double *__restrict__ xb,
     const double *__restrict__ gb, const LcpState *__restrict__ st, const double *__restrict__ xscale,
     double *__restrict__ U, double *__restrict__ Fout, const double *__restrict__ Fa) {
@@ -666,8 +673,8 @@ int op_scatter(relcp_ctx *ctx, int64_t nb, const double *x, const double *g, int
     if (!ctx->op_sorted) bpw = 32;
     const int64_t nwarp = (nb + bpw - 1) / bpw;
     int64_t grid = (nwarp + SCATTER_WPB - 1) / SCATTER_WPB;
-    if (grid > (int64_t)RELCP_SM_COUNT * SCATTER_MINB * SCATTER_WAVES)
-        grid = (int64_t)RELCP_SM_COUNT * SCATTER_MINB * SCATTER_WAVES;
+    const int64_t gcap = (int64_t)RELCP_SM_COUNT * (bpw == 32 ? SCATTER_MINB32 : SCATTER_MINB) * SCATTER_WAVES;
+    if (grid > gcap) grid = gcap;
     if (grid < 1) grid = 1;
     const unsigned G = (unsigned)grid, T = 32 * SCATTER_WPB;
     const int *pa = ctx->pa.p;
