@@ -835,10 +835,14 @@ int op_fused_rows(relcp_ctx *ctx, const relcp_constraints *cs, int64_t nb, doubl
 
 // ------------------------------------------------------------ gather
 #ifndef GATHER_ILP
-#define GATHER_ILP 2  // rows per thread per trip in the apply gather (same-box A/B with compact rows: 2 beats 4)
+#define GATHER_ILP 2  // rows per thread per trip in the apply gather (store rows; same-box A/B: 2 beats 4)
 #endif
+#ifndef GATHER_ILP_CR
+#define GATHER_ILP_CR 1  // with compact rows: 1 row x 4 blocks (64 registers).  Same-box A/B, whole apply on cfg5
+#endif                   // A_0 / the relaxed store (us): 227.8 / 285.0 against 232.6 / 293.1 (2 rows x 3 blocks,
+                         // 72 registers), 233.7 / 294.4 (1 x 3), 244.0 / 309.6 (2 x 2)
 #ifndef GATHER_MINB_CR
-#define GATHER_MINB_CR 3  // resident blocks per SM with compact rows (register budget 80)
+#define GATHER_MINB_CR 4  // resident blocks per SM with compact rows
 #endif
 
 // y = scale * D^T U ; optionally the grid-wide ||y||^2 -> st->pnorm = 1/||y||, st->L = ||y||
@@ -854,18 +858,19 @@ __global__ void __launch_bounds__(RELCP_NT, CR ? GATHER_MINB_CR : 4) k_gather(in
                                                      unsigned *counter, LcpState *st, double *acc_out,
                                                      const int *__restrict__ yperm) {
     __shared__ double sh[32];
+    constexpr int ILP = CR ? GATHER_ILP_CR : GATHER_ILP;
     double acc[1] = {0.0};
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t a0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a0 < nc; a0 += GATHER_ILP * stride) {
-        double v[GATHER_ILP];
+    for (int64_t a0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a0 < nc; a0 += ILP * stride) {
+        double v[ILP];
 #pragma unroll
-        for (int u = 0; u < GATHER_ILP; ++u) {
+        for (int u = 0; u < ILP; ++u) {
             const int64_t a = a0 + u * stride;
             const int64_t ac = a < nc ? a : a0;
             v[u] = scale * (CR ? row_dot_c(ac, rs, ia, ib, rc, U) : row_dot(ac, cap, ia, ib, n, ta, tb, U));
         }
 #pragma unroll
-        for (int u = 0; u < GATHER_ILP; ++u) {
+        for (int u = 0; u < ILP; ++u) {
             const int64_t a = a0 + u * stride;
             if (a >= nc) continue;
             y[yperm ? yperm[a] : a] = v[u];  // JDS operator, caller's store order: slot -> row
